@@ -1,0 +1,168 @@
+"""Batched TE-PAI ensemble on the B200 engine (north_star items 1-4).
+
+Host: the reference-identical sampler draws every circuit (``circuit_stream``
+keyed by sample id, so the draw is independent of batching and rank count),
+``packing`` turns it into gate words, and one ``tb_run_ensemble`` call runs the
+persistent kernel over the whole batch.  Multi-GPU: one process per GPU, each
+rank takes a contiguous range of sample ids, and the fixed-point (checkpoint,
+site) sums are combined with a single ``all_reduce`` — the only collective of
+the path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .estimator import aggregate_fixed
+from .mps import SITE_VECTORS, TruncationPolicy
+from .packing import TermTable, angle_table, pack_batch, pack_sampled, tepai_angles
+from .pauli import Hamiltonian
+from .rng import circuit_stream
+from .sampling import PaiConfig, circuit_weight_norm, sample_circuit
+
+
+def checkpoint_weights(ham: Hamiltonian, cfg: PaiConfig, checkpoints) -> np.ndarray:
+    """||g||_1 of each prefix: circuit_weight_norm(H, PaiConfig(D, j, jT/N))
+    (SURVEY.md §8(a) prefix semantics)."""
+    return np.array([circuit_weight_norm(ham, PaiConfig(cfg.delta, int(j), j * cfg.total_time / cfg.n_steps, cfg.mode))
+                     for j in checkpoints])
+
+
+@dataclass
+class PackedEnsemble:
+    """Host-side input of one engine call."""
+
+    n: int
+    cap: int
+    chi_cut: int
+    floor: float
+    words: np.ndarray
+    offsets: np.ndarray
+    ckpt_end: np.ndarray
+    ckpt_sign: np.ndarray
+    angle_cs: np.ndarray
+    weights: np.ndarray
+    obs_sites: np.ndarray
+    init_vecs: np.ndarray
+    sample_ids: np.ndarray
+    nu: np.ndarray
+    pi_local: bool = True
+
+    @property
+    def n_samples(self) -> int:
+        return int(self.sample_ids.size)
+
+    def nbytes(self) -> int:
+        return sum(a.nbytes for a in (self.words, self.offsets, self.ckpt_end, self.ckpt_sign, self.angle_cs,
+                                      self.obs_sites, self.init_vecs))
+
+
+def pack_ensemble(ham: Hamiltonian, cfg: PaiConfig, seed: int, sample_ids, labels, policy: TruncationPolicy,
+                  checkpoints, obs_sites=None, pi_local: bool = True) -> PackedEnsemble:
+    """Sample (reference-identical draws) and pack a batch of circuits."""
+    n = ham.n
+    if len(labels) != n:
+        raise ValueError("initial-state labels do not match the chain length")
+    hard = 2 ** (n // 2)
+    cut = hard if policy.chi_cut is None else min(policy.chi_cut, hard)
+    checkpoints = np.asarray(checkpoints, dtype=np.int64)
+    if checkpoints.size and (np.any(np.diff(checkpoints) <= 0) or checkpoints[0] < 0 or checkpoints[-1] > cfg.n_steps):
+        raise ValueError("checkpoints must be increasing step counts within [0, n_steps]")
+    table = TermTable.of(ham)
+    ids = np.asarray(list(sample_ids), dtype=np.int64)
+    packed = []
+    for sid in ids:
+        circ = sample_circuit(ham, cfg, circuit_stream(seed, int(sid)), sample_id=int(sid))
+        packed.append(pack_sampled(circ, table, checkpoints))
+    words, offs, ce, cs = pack_batch(packed, int(checkpoints.size))
+    obs = np.arange(n, dtype=np.int32) if obs_sites is None else np.asarray(obs_sites, dtype=np.int32)
+    init = np.stack([SITE_VECTORS[lab] for lab in labels]).astype(np.complex128)
+    return PackedEnsemble(n, cut, cut, float(policy.svalue_floor), words, offs, ce, cs,
+                          angle_table(tepai_angles(cfg.delta)), checkpoint_weights(ham, cfg, checkpoints), obs,
+                          init.view(np.float64).reshape(n, 4).copy(), ids, np.diff(offs), pi_local)
+
+
+@dataclass
+class EnsembleRun:
+    """Per-sample outputs and fixed-point sums of one (or several merged) calls."""
+
+    n_samples: int
+    values: np.ndarray | None     # [S, C, O] raw <Z_j>
+    discarded: np.ndarray | None  # [S, C]
+    ledger: np.ndarray | None     # [S, 4]
+    sum_v: np.ndarray             # int64 [C, O]
+    sum_v2: np.ndarray            # int64 [C, O]
+    weights: np.ndarray           # [C]
+    flops: float
+    kernel_ms: float
+    wall_s: float
+    extra: dict = field(default_factory=dict)
+
+    def stats(self) -> dict:
+        return aggregate_fixed(self.sum_v, self.sum_v2, self.n_samples, self.weights)
+
+
+def run_packed(p: PackedEnsemble, device: int = 0, keep_values: bool = True) -> EnsembleRun:
+    """One end-to-end engine call with host buffers (``tb_run_ensemble``)."""
+    S, C, O = p.n_samples, p.ckpt_end.shape[1] if p.ckpt_end.ndim == 2 else 0, p.obs_sites.size
+    values = np.zeros((S, C, O)) if keep_values else None
+    disc = np.zeros((S, C)) if keep_values else None
+    ledger = np.zeros((S, 4))
+    sv = np.zeros((C, O), np.int64)
+    sv2 = np.zeros((C, O), np.int64)
+    flops = np.zeros(1)
+    kms = np.zeros(1, np.float32)
+    arrays = [np.ascontiguousarray(x) for x in (p.words, p.offsets, p.ckpt_end, p.ckpt_sign, p.angle_cs,
+                                                 p.weights, p.obs_sites, p.init_vecs)]
+    w, off, ce, cs, ang, wt, obs, iv = arrays
+    desc = _lib.EnsembleDesc(p.n, p.cap, p.chi_cut, int(p.pi_local), p.floor, S, C, O, ang.shape[0],
+                             w.ctypes.data, off.ctypes.data, ce.ctypes.data, cs.ctypes.data, ang.ctypes.data,
+                             wt.ctypes.data, obs.ctypes.data, iv.ctypes.data)
+    out = _lib.EnsembleOut(values.ctypes.data if values is not None else None,
+                           disc.ctypes.data if disc is not None else None, ledger.ctypes.data,
+                           sv.ctypes.data, sv2.ctypes.data, flops.ctypes.data, kms.ctypes.data)
+    ctx = _lib.context(device)
+    t0 = time.perf_counter()
+    _lib.check(_lib.load().tb_run_ensemble(ctx, ctypes.byref(desc), ctypes.byref(out)), ctx)
+    wall = time.perf_counter() - t0
+    return EnsembleRun(S, values, disc, ledger, sv, sv2, p.weights, float(flops[0]), float(kms[0]), wall)
+
+
+def run_ensemble(ham: Hamiltonian, cfg: PaiConfig, seed: int, sample_ids, init_labels, policy: TruncationPolicy,
+                 checkpoints, observables=None, pi_local: bool = True, device: int = 0,
+                 keep_values: bool = True) -> EnsembleRun:
+    """Batched ensemble: <Z_j> at each checkpoint step for every sample, plus the
+    signed fixed-point sums of the estimator."""
+    p = pack_ensemble(ham, cfg, seed, sample_ids, init_labels, policy, checkpoints, observables, pi_local)
+    return run_packed(p, device, keep_values)
+
+
+def shard_range(n_samples: int, rank: int, world: int) -> range:
+    """Contiguous sample-id range of one rank."""
+    lo = (n_samples * rank) // world
+    hi = (n_samples * (rank + 1)) // world
+    return range(lo, hi)
+
+
+def allreduce_sums(run: EnsembleRun, group=None) -> EnsembleRun:
+    """Combine per-rank fixed-point sums with ONE all_reduce (int64, exact and
+    order-independent).  Packs [sum_v, sum_v2, n_samples] in one tensor."""
+    import torch
+    import torch.distributed as dist
+
+    C, O = run.sum_v.shape
+    flat = np.concatenate([run.sum_v.ravel(), run.sum_v2.ravel(), np.array([run.n_samples], np.int64)])
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.from_numpy(flat).to(dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    t = t.cpu().numpy()
+    return EnsembleRun(int(t[-1]), None, None, None, t[: C * O].reshape(C, O).copy(),
+                       t[C * O: 2 * C * O].reshape(C, O).copy(), run.weights, run.flops, run.kernel_ms,
+                       run.wall_s, dict(run.extra))

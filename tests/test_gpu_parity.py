@@ -1,0 +1,210 @@
+"""GPU parity tests: the CUDA engine (through the C ABI) against the CPU oracle
+and the reference-generated golden fixtures.
+
+Tolerances (north_star): untruncated <= 1e-10 (absolute on
+<Z> in [-1, 1]); truncated regime per sample <= 1e-8 only while the
+cumulative discarded weight is tiny; gauge-dependent tensors are compared
+through gauge-invariant quantities (expectations, state vectors, singular
+values)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2604_13144_b200 as tb
+from oracle.mps_oracle import OracleMPS, run_sample_checkpoints
+
+pytestmark = pytest.mark.gpu
+DELTA = math.pi / 2**7
+
+
+def _svd_gpu(engine, a):
+    lib, ctx = engine.load(), engine.context(0)
+    b, m, n = a.shape
+    k = min(m, n)
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    s = np.zeros((b, k))
+    u = np.zeros((b, m, k), np.complex128)
+    vh = np.zeros((b, k, n), np.complex128)
+    engine.check(lib.tb_svd(ctx, a.ctypes.data, b, m, n, s.ctypes.data, u.ctypes.data, vh.ctypes.data), ctx)
+    return u, s, vh
+
+
+@pytest.mark.parametrize("m,n", [(2, 2), (4, 16), (16, 4), (32, 32), (64, 128), (128, 64), (128, 128), (256, 256)])
+def test_jacobi_svd_matches_lapack(engine, m, n):
+    rng = np.random.default_rng(m * 1000 + n)
+    k = min(m, n)
+    # graded spectrum down to 1e-14 plus an exactly rank-deficient tail
+    q1, _ = np.linalg.qr(rng.normal(size=(m, k)) + 1j * rng.normal(size=(m, k)))
+    q2, _ = np.linalg.qr(rng.normal(size=(n, k)) + 1j * rng.normal(size=(n, k)))
+    sv = np.logspace(0, -14, k)
+    sv[-(k // 8):] = 0.0
+    a = np.stack([(q1 * sv) @ q2.conj().T, rng.normal(size=(m, n)) + 1j * rng.normal(size=(m, n))])
+    u, s, vh = _svd_gpu(engine, a)
+    for b in range(2):
+        ref = np.linalg.svd(a[b], compute_uv=False)
+        np.testing.assert_allclose(s[b] / ref[0], ref / ref[0], rtol=0, atol=2e-14)
+        rec = (u[b] * s[b]) @ vh[b]
+        assert np.linalg.norm(rec - a[b]) <= 1e-12 * np.linalg.norm(a[b])
+        live = s[b] > 1e-10 * s[b][0]
+        uu = u[b][:, live]
+        assert np.abs(uu.conj().T @ uu - np.eye(uu.shape[1])).max() < 1e-12
+
+
+def test_single_gate_known_answers(engine, golden):
+    kat = golden("ref_kat.npz")
+    st = tb.init_product_state("+++")
+    tb.apply_pauli_rotation(st, tb.PauliString.from_label("Z0Z1", 3), math.pi / 2, tb.TruncationPolicy(16))
+    assert abs(tb.expectation(st, tb.PauliString.from_label("X0", 3)) - float(kat["zz_x0"])) < 1e-14
+    assert st.bond_dims == tuple(kat["zz_bonds"])
+    st = tb.init_product_state("00")
+    tb.apply_pauli_rotation(st, tb.PauliString.from_label("X0", 2), math.pi, tb.TruncationPolicy(16))
+    assert tb.expectation(st, tb.PauliString.from_label("Z0", 2)) == pytest.approx(-1.0, abs=1e-15)
+    # identity-angle gate: state and ledger unchanged
+    led = tb.CostLedger()
+    before = st.buf.copy()
+    tb.apply_pauli_rotation(st, tb.PauliString.from_label("X0X1", 2), 0.0, tb.TruncationPolicy(16), led)
+    assert led.gate_count == 0 and np.array_equal(before, st.buf)
+
+
+def test_ring_swap_network_statevector(engine, golden):
+    kat = golden("ref_kat.npz")
+    ham = tb.build_spin_ring(6, 1.0, 11)
+    st = tb.init_product_state("0+1-0+")
+    for k, t in enumerate(ham.terms):
+        tb.apply_pauli_rotation(st, t.pauli, 0.3 + 0.01 * k, tb.EXACT)
+    assert st.bond_dims == tuple(kat["ring6_dims"])
+    np.testing.assert_allclose(st.to_statevector(), kat["ring6_psi"], atol=1e-12)
+
+
+def test_run_circuit_statevector_vs_reference(engine, golden):
+    ref = golden("ref_c1.npz")
+    ham = tb.build_spin_ring(8, 1.0, 0)
+    cfg = tb.PaiConfig(DELTA, 100, 1.0)
+    for i in range(4):
+        circ = tb.sample_circuit(ham, cfg, tb.circuit_stream(1, i), sample_id=i)
+        st = tb.init_product_state("01" * 4)
+        led = tb.CostLedger()
+        tb.run_circuit(st, circ, tb.TruncationPolicy(16), led)
+        np.testing.assert_allclose(st.to_statevector(), ref["psi"][i], atol=1e-10)
+        assert abs(tb.expectation(st, tb.PauliString(8)) - 1.0) < 1e-12  # norm
+        # whole-circuit call: the ledger's sum of kept-bond cubes obeys the SPEC bound
+        assert led.sum_chi_cubed <= led.gate_count * led.chi_max**3
+
+
+def test_general_pauli_expectation(engine):
+    ham = tb.build_spin_ring(7, 1.0, 2)
+    st = tb.init_product_state("0+1-01+")
+    ora = OracleMPS("0+1-01+")
+    ops = [(t.pauli, 0.37 + 0.05 * k) for k, t in enumerate(ham.terms)]
+    tb.run_circuit(st, _OpsCircuit(7, ops), tb.EXACT)
+    ora.run(ops, None, 1e-14)
+    for label in ("X0", "Y3", "Z6", "X1Y2Z5", "Y0Y6", "Z0Z1Z2Z3Z4Z5Z6"):
+        p = tb.PauliString.from_label(label, 7)
+        assert tb.expectation(st, p) == pytest.approx(ora.expect(dict((s, y) for s, y in p.ops)), abs=1e-12)
+
+
+class _OpsCircuit:
+    def __init__(self, n, ops):
+        self.n, self._ops = n, ops
+
+    def operations(self):
+        return iter(self._ops)
+
+
+def test_rank_deficient_centre_move_zero_padded(engine):
+    """2*cl < cr on a centre move: the reference fails in a reshape
+    (_kernel.py:75); both the oracle and the engine zero-pad."""
+    rng = np.random.default_rng(5)
+    dims = [1, 1, 4, 2, 1]
+    st = tb.MPSState(4)
+    st.ensure_capacity(4)
+    st.dims = np.array(dims, np.int64)
+    ora = OracleMPS("0000")
+    ora.grow(4)
+    ora.dims = np.array(dims, np.int64)
+    for s in range(4):
+        t = rng.normal(size=(dims[s], 2, dims[s + 1])) + 1j * rng.normal(size=(dims[s], 2, dims[s + 1]))
+        st.buf[s, : dims[s], :, : dims[s + 1]] = t
+        ora.buf[s, : dims[s], :, : dims[s + 1]] = t
+    nrm = math.sqrt(abs(tb.expectation(st, tb.PauliString(4))))
+    st.buf[0] /= nrm
+    ora.buf[0] /= nrm
+    ops = [(tb.PauliString.from_label("X2Y3", 4), 0.4)]
+    tb.run_circuit(st, _OpsCircuit(4, ops), tb.TruncationPolicy(4, 1e-14))
+    ora.run(ops, 4, 1e-14)
+    for j in range(4):
+        p = tb.PauliString.single(4, j, "Z")
+        assert tb.expectation(st, p) == pytest.approx(ora.expect({j: "Z"}), abs=1e-12)
+
+
+@pytest.mark.parametrize("pi_local", [False, True])
+def test_c1_ensemble_per_sample_parity(engine, golden, pi_local):
+    """Config 1 (untruncated): every sample, every checkpoint, every site vs the
+    reference run on the same gate lists, <= 1e-10."""
+    ref = golden("ref_c1.npz")
+    ham = tb.build_spin_ring(8, 1.0, 0)
+    cfg = tb.PaiConfig(DELTA, 100, 1.0)
+    ids = ref["full_ids"][:64]
+    run = tb.run_ensemble(ham, cfg, 1, ids, "01" * 4, tb.TruncationPolicy(16), ref["checkpoints"], pi_local=pi_local)
+    np.testing.assert_allclose(run.values, ref["vals_full"][: len(ids)], rtol=0, atol=1e-10)
+    if not pi_local:
+        np.testing.assert_array_equal(run.ledger[:, 0], ref["ledger"][: len(ids), 0])
+        np.testing.assert_array_equal(run.ledger[:, 1], ref["ledger"][: len(ids), 1])
+    # fused fixed-point sums == host quantisation of sign * <Z>
+    signs = ref["sign"][: len(ids)].astype(np.float64)
+    want_v = tb.estimator.quantize(signs[:, :, None] * run.values).sum(axis=0)
+    want_v2 = tb.estimator.quantize(run.values**2).sum(axis=0)
+    np.testing.assert_array_equal(run.sum_v, want_v)
+    np.testing.assert_array_equal(run.sum_v2, want_v2)
+
+
+def test_c1_estimator_vs_reference_mean(engine, golden):
+    """1,000-sample Z_0 estimate equals the mean of the reference's per-sample
+    signed, weighted values (same circuits) to 1e-10."""
+    ref = golden("ref_c1.npz")
+    ham = tb.build_spin_ring(8, 1.0, 0)
+    cfg = tb.PaiConfig(DELTA, 100, 1.0)
+    run = tb.run_ensemble(ham, cfg, 1, range(1000), "01" * 4, tb.TruncationPolicy(16), ref["checkpoints"],
+                          observables=[0], keep_values=True)
+    st = run.stats()
+    want = ref["weights"] * np.mean(ref["sign"] * ref["z0"], axis=0)
+    np.testing.assert_allclose(st["estimate"][:, 0], want, atol=1e-10)
+    np.testing.assert_allclose(run.values[:, :, 0], ref["z0"], atol=1e-10)
+
+
+def test_c2_truncated_prefix_parity(engine, golden):
+    ref = golden("ref_c2.npz")
+    ham = tb.build_spin_ring(16, 1.0, 2)
+    cfg = tb.PaiConfig(DELTA, 200, 2.0)
+    ck = ref["checkpoints"][:4]
+    run = tb.run_ensemble(ham, cfg, 3, range(4), "01" * 8, tb.TruncationPolicy(32, 1e-12), ck, pi_local=False)
+    for i in range(4):
+        ok = ref["disc"][i][:4] < 1e-7
+        np.testing.assert_allclose(run.values[i][ok], ref["vals_full"][i][:4][ok], atol=1e-8)
+        np.testing.assert_allclose(run.discarded[i][ok], ref["disc"][i][:4][ok], rtol=1e-3, atol=1e-15)
+
+
+def test_c3_headline_prefix_parity(engine, golden):
+    ref = golden("ref_c3.npz")
+    ham = tb.build_spin_ring(32, 1.0, 4)
+    cfg = tb.PaiConfig(DELTA, 200, 2.0)
+    ck = ref["checkpoints"]
+    run = tb.run_ensemble(ham, cfg, 5, range(2), "01" * 16, tb.TruncationPolicy(64, 1e-12), ck, pi_local=False)
+    for i in range(2):
+        np.testing.assert_allclose(run.values[i], ref["vals_full"][i], atol=1e-8)
+        np.testing.assert_allclose(run.discarded[i], ref["disc"][i], rtol=1e-2, atol=1e-14)
+
+
+def test_empty_and_degenerate_inputs(engine):
+    st = tb.init_product_state("0101")
+    before = st.buf.copy()
+    tb.run_circuit(st, _OpsCircuit(4, []), tb.TruncationPolicy(4))
+    assert np.array_equal(before, st.buf)
+    ham = tb.build_spin_ring(4, 1.0, 0)
+    cfg = tb.PaiConfig(DELTA, 5, 0.0)  # T = 0: no non-identity draws
+    run = tb.run_ensemble(ham, cfg, 0, range(3), "0101", tb.TruncationPolicy(4), [5])
+    np.testing.assert_allclose(run.values[:, 0, :], np.tile([1, -1, 1, -1], (3, 1)), atol=0)
+    run = tb.run_ensemble(ham, tb.PaiConfig(DELTA, 10, 0.1), 0, [], "0101", tb.TruncationPolicy(4), [5])
+    assert run.n_samples == 0

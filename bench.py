@@ -1,0 +1,287 @@
+"""Benchmark: TE-PAI circuit samples/sec on config 3 (N=32 disordered
+Heisenberg ring, chi=64, complex128) and the % of the FP64 roofline.
+
+A *step* is one pass of the hot path over one batch: every in-flight circuit
+(one persistent slot per SM, 148 on a B200) advances by one checkpoint
+segment (10 of its 200 Trotter steps) and its <Z_j> are measured and added to
+the signed estimator sums; a slot whose circuit finished restarts with the
+next sample id (continuous batching).  20 steps = one full circuit per slot,
+so samples/s = slots * K / 20 / T (sample-equivalents).  All slots start at
+step 0, so the default window (W=3, K=17) is segments 3..19 of the first
+circuits — it omits the cheap bond-growth segments and therefore
+under-states the throughput of complete circuits.
+
+``value`` uses the device time of the K persistent-kernel launches (inputs
+already in HBM when each launch starts); ``e2e`` is the wall time of the same
+K steps through the host-buffer C ABI call ``tb_step`` (H2D of the step's gate
+words, D2H of <Z_j> and sums, inside the timed region).
+
+``--impl reference`` times the CPU path instead: the numpy port of the
+reference engine (oracle/, same LAPACK calls), one process per host core,
+each advancing its own circuit by one segment per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+# one BLAS thread per process: the CPU arm forks one worker per core, and a
+# multithreaded BLAS inherited across fork would oversubscribe the host
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+os.environ.setdefault("MKL_NUM_THREADS", "1")
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TE-PAI circuit samples/sec (N=32, χ=64, complex128) and % of FP64 roofline"
+UNIT = "samples/s"
+FP64_PEAK_TFLOPS = 37.08  # measured DMMA rate on this pool's B200 (profiles/r01_fp64_peak.txt)
+C3 = dict(n=32, chi=64, ham_seed=4, circ_seed=5, n_steps=200, total_time=2.0, every=10)
+WORKLOAD = ("C3: N=32 periodic disordered Heisenberg ring (h_j~U[-1,1], seed 4), Neel state, T=2.0 in 200 "
+            "Trotter steps, Delta=pi/2^7, circuits from seed 5, chi_max=64, floor 1e-12, <Z_j> all j at 20 checkpoints")
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > i + 2 and r[i + 2] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def c3_objects():
+    import paper_2604_13144_b200 as tb
+
+    ham = tb.build_spin_ring(C3["n"], 1.0, C3["ham_seed"])
+    cfg = tb.PaiConfig(math.pi / 2**7, C3["n_steps"], C3["total_time"])
+    pol = tb.TruncationPolicy(chi_cut=C3["chi"], svalue_floor=1e-12)
+    ck = np.arange(C3["every"], C3["n_steps"] + 1, C3["every"])
+    return tb, ham, cfg, pol, ck
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: numpy port of the reference engine (oracle/), one process per core
+# ---------------------------------------------------------------------------
+def _cpu_worker(args):
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+    sid, n_segments, conn = args
+    tb, ham, cfg, pol, ck = c3_objects()
+    from oracle.mps_oracle import OracleMPS
+
+    circ = tb.sample_circuit(ham, cfg, tb.circuit_stream(C3["circ_seed"], sid), sample_id=sid)
+    st = OracleMPS("01" * (C3["n"] // 2))
+    times, lo = [], 0
+    for c in range(n_segments):
+        hi = int(np.searchsorted(circ.step_index, ck[c % ck.size]))
+        if c % ck.size == 0:
+            st, lo = OracleMPS("01" * (C3["n"] // 2)), 0
+        t0 = time.perf_counter()
+        st.run(circ.slice_entries(lo, hi).operations(), C3["chi"], 1e-12)
+        _ = [st.expect({j: "Z"}) for j in range(C3["n"])]
+        times.append(time.perf_counter() - t0)
+        lo = hi
+    return times
+
+
+def cpu_segments(n_segments: int, cores: int):
+    """Each of `cores` processes advances its own circuit by n_segments
+    checkpoint segments; returns the per-step wall times (max over cores)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, [(i, n_segments, None) for i in range(cores)])
+        wall = time.perf_counter() - t0
+    per_step = np.max(np.array(res), axis=0)
+    return per_step, wall
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    cores = host_cores()
+    steps = args.warmup + args.steps
+    per_step, wall = cpu_segments(steps, cores)
+    timed = float(np.sum(per_step[args.warmup:]))
+    value = cores * args.steps / 20.0 / timed
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * timed / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (reference sampler, seeded)",
+        "config": {"workload": WORKLOAD, "step": "one checkpoint segment (10 Trotter steps) per in-flight circuit",
+                   "slots": cores, "parallelism": f"{cores} CPU processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{cores} circuits x {steps} checkpoint segments (numpy port of the reference "
+                                   f"engine, zgesdd via numpy LAPACK, 1 thread per process)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2604_13144_b200 import _lib
+    from paper_2604_13144_b200.ensemble import SlotPipeline
+
+    tb, ham, cfg, pol, ck = c3_objects()
+    pipe = SlotPipeline(ham, cfg, C3["circ_seed"], "01" * (C3["n"] // 2), pol, ck, n_slots=args.slots,
+                        device=local, first_sample=rank, sample_stride=world)
+    S = pipe.n_slots
+    plans = [pipe.plan() for _ in range(args.warmup + args.steps)]
+    h2d = [sum(x.nbytes for x in (p.words, p.offsets, p.ckpt_end, p.ckpt_sign, p.reset, p.sum_row)) for p in plans]
+    d2h = S * C3["n"] * 8 + 2 * pipe.sum_v.nbytes
+    for i, p in enumerate(plans[: args.warmup]):
+        ms = pipe.step_host(p)
+        print(f"[bench] warmup step {i}: {ms:.0f} ms", file=sys.stderr, flush=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kernel_ms, flops0 = [], pipe.flops
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i, p in enumerate(plans[args.warmup:]):
+            kernel_ms.append(pipe.step_host(p))
+            print(f"[bench] step {i}: {kernel_ms[-1]:.0f} ms", file=sys.stderr, flush=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            sums = torch.from_numpy(np.concatenate([pipe.sum_v.ravel(), pipe.sum_v2.ravel()])).cuda()
+            dist.all_reduce(sums)  # the path's only collective: estimator sums
+        wall = time.perf_counter() - t0
+    dev_s = sum(kernel_ms) / 1e3
+    flops = pipe.flops - flops0
+    if world > 1:
+        t = torch.tensor([dev_s, wall], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s, wall = float(t[0]), float(t[1])
+        f = torch.tensor([flops], dtype=torch.float64, device="cuda")
+        dist.all_reduce(f)
+        flops = float(f[0])
+    samples = world * S * args.steps / 20.0
+    value = samples / dev_s
+    e2e = samples / wall
+    achieved = flops / dev_s / 1e12 / world  # per GPU, dominant kernel = the persistent ensemble kernel
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (reference-identical seeded sampler, random disorder seed 4)",
+        "config": {"workload": WORKLOAD, "slots_per_gpu": S,
+                   "step": "one checkpoint segment (10 Trotter steps) of every in-flight circuit",
+                   "samples_per_step": S / 20.0, "l2": "resident MPS state %.0f MB per GPU > 126 MB L2" % (
+                       S * C3["n"] * 64 * 2 * 64 * 16 / 1e6),
+                   "parallelism": f"dp{world} (sample sharding, one NCCL all_reduce of the estimator sums)"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "peak_source": "measured FP64 DMMA rate (MEASURED_PEAKS.json has no FP64 entry)",
+                     "flops": "SURVEY.md §8(d) algorithmic count (two-site contraction + LAPACK-nominal SVD + QR moves)"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(np.mean(h2d[args.warmup:])),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        per_step, _ = cpu_segments(args.cpu_segments, cores)
+        cpu = cores * args.cpu_segments / 20.0 / float(np.sum(per_step))
+        line["cpu_baseline"] = {"value": cpu, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"{cores} circuits x first {args.cpu_segments} checkpoint segments (cheap "
+                                          "bond-growth phase, so this over-states the CPU rate)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=17)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--slots", type=int, default=None)
+    ap.add_argument("--cpu-segments", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -52,6 +52,12 @@ void tb_destroy(tb_ctx* ctx);
 const char* tb_last_error(const tb_ctx* ctx);
 /* Number of SMs of the bound device (persistent-grid size). */
 int tb_num_sms(const tb_ctx* ctx);
+/* Diagnostics: clock64 phase counters of the last ensemble launch, summed over
+ * CTAs: [0] Jacobi cycles [1] Jacobi calls [2] sweeps [3] centre moves
+ * [4] contraction+gate [5] sort+split write-back [6] <Z> sweeps
+ * [7] per-sample totals [9..11] cycles/calls/sweeps of 128x128 problems,
+ * [16+k] rotations applied in sweep k.  out must hold 64 entries. */
+int tb_debug_profile(tb_ctx* ctx, uint64_t* out64);
 
 /* Drop-in for _kernel.run_stream: executes the lowered stream on one MPS.
  * buf: complex128 [n][cap][2][cap] (mutated); dims: int64 [n+1] (mutated);
@@ -111,6 +117,26 @@ int tb_run_ensemble(tb_ctx* ctx, const tb_ensemble_desc* desc, tb_ensemble_out* 
  * (kernel_ms may be a host pointer or NULL); runs on `stream` (cudaStream_t,
  * NULL = legacy default) and does not synchronize unless kernel_ms != NULL. */
 int tb_run_ensemble_device(tb_ctx* ctx, const tb_ensemble_desc* desc, tb_ensemble_out* out, void* stream);
+
+/* Continuous batching ("slots"): one persistent CTA per slot keeps that
+ * slot's MPS resident in HBM between calls.  Each call advances every slot
+ * by its own gate-stream segment (base.gates / gate_offsets indexed by slot),
+ * optionally restarting it from the product state first (reset[slot] = 1),
+ * measures <Z_j> at the segment's checkpoints and adds the signed fixed-point
+ * values to estimator row sum_row[slot][c].  The first call for a given
+ * (n, cap, n_slots) must reset every slot; any other engine call on the same
+ * context (run_stream, run_ensemble, svd) invalidates the slot states.
+ * n_slots (= base.n_samples) must not exceed tb_num_sms(). */
+typedef struct tb_step_desc {
+  tb_ensemble_desc base;
+  const uint8_t* reset;    /* [n_slots] */
+  const int32_t* sum_row;  /* [n_slots][n_ckpt] */
+} tb_step_desc;
+
+/* host buffers; sum_v/sum_v2 hold sum_rows x n_obs entries */
+int tb_step(tb_ctx* ctx, const tb_step_desc* desc, tb_ensemble_out* out, int64_t sum_rows);
+/* device buffers on `stream` */
+int tb_step_device(tb_ctx* ctx, const tb_step_desc* desc, tb_ensemble_out* out, void* stream);
 
 #ifdef __cplusplus
 }

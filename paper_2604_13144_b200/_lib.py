@@ -14,8 +14,8 @@ LIB_NAME = "libtepai_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 EXPORTED = (
-    "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_run_stream",
-    "tb_expectation", "tb_svd", "tb_run_ensemble", "tb_run_ensemble_device",
+    "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_debug_profile", "tb_run_stream",
+    "tb_expectation", "tb_svd", "tb_run_ensemble", "tb_run_ensemble_device", "tb_step", "tb_step_device",
 )
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -42,6 +42,10 @@ class EnsembleOut(ctypes.Structure):
     ]
 
 
+class StepDesc(ctypes.Structure):
+    _fields_ = [("base", EnsembleDesc), ("reset", ctypes.c_void_p), ("sum_row", ctypes.c_void_p)]
+
+
 _lock = threading.Lock()
 _lib = None
 _ctxs: dict[int, ctypes.c_void_p] = {}
@@ -64,11 +68,14 @@ def load() -> ctypes.CDLL:
         lib.tb_last_error.argtypes = [vp]
         lib.tb_last_error.restype = ctypes.c_char_p
         lib.tb_num_sms.argtypes = [vp]
+        lib.tb_debug_profile.argtypes = [vp, vp]
         lib.tb_run_stream.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp, vp, vp, i64, i64, dbl, vp, vp]
         lib.tb_expectation.argtypes = [vp, vp, i64, i64, vp, vp, vp]
         lib.tb_svd.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp]
         lib.tb_run_ensemble.argtypes = [vp, ctypes.POINTER(EnsembleDesc), ctypes.POINTER(EnsembleOut)]
         lib.tb_run_ensemble_device.argtypes = [vp, ctypes.POINTER(EnsembleDesc), ctypes.POINTER(EnsembleOut), vp]
+        lib.tb_step.argtypes = [vp, ctypes.POINTER(StepDesc), ctypes.POINTER(EnsembleOut), i64]
+        lib.tb_step_device.argtypes = [vp, ctypes.POINTER(StepDesc), ctypes.POINTER(EnsembleOut), vp]
         _lib = lib
         return lib
 
@@ -98,3 +105,11 @@ def check(rc: int, ctx) -> None:
 
 def ptr(a: np.ndarray) -> int:
     return a.ctypes.data if a is not None else None
+
+
+def debug_profile(device: int = 0) -> np.ndarray:
+    """Phase cycle counters of the last ensemble launch (see tb_debug_profile)."""
+    out = np.zeros(64, np.uint64)
+    ctx = context(device)
+    check(load().tb_debug_profile(ctx, out.ctypes.data), ctx)
+    return out

@@ -83,7 +83,10 @@ struct Job {
   const int8_t* ckpt_sign;
   const double* angle_cs;
   const int32_t* obs_sites;
-  const double* init_vecs;  // NULL => state preloaded in slot 0 (run_stream mode)
+  const double* init_vecs;  // product-state site vectors [n][2] (complex)
+  int slot_mode;            // 0: work queue of whole samples; 1: CTA b advances slot b
+  const uint8_t* reset;     // slot mode: 1 = start slot b from the product state (NULL: never)
+  const int32_t* sum_row;   // [n_samples][n_ckpt] estimator row of each checkpoint (NULL: ck)
   // outputs
   double* values;
   double* discarded;
@@ -91,12 +94,13 @@ struct Job {
   unsigned long long* sum_v;
   unsigned long long* sum_v2;
   double* flops;       // [gridDim.x]
+  unsigned long long* prof;  // [16] clock64 phase counters (diagnostics)
   int* next_sample;
   int* status;         // bit 0: Jacobi non-convergence, bit 1: bad dims
   // run_stream mode i/o
-  int* io_dims;        // [n+1]
-  int* io_center;
-  double* io_counters; // [4] in/out
+  int* slot_dims;        // [grid][MAXN+1] persistent slot state (slot mode)
+  int* slot_center;      // [grid]
+  double* slot_counters; // [grid][4]
   // workspace
   double2* ws_mps;
   double2* ws_W;
@@ -108,6 +112,7 @@ struct Job {
 struct Smem {
   int dims[MAXN + 1];
   double sig[MAXDIM];
+  double nrm[4 * 32];
   int perm[MAXDIM];
   double2 rco[MAXDIM];
   double red[NWARP * 4];
@@ -117,6 +122,9 @@ struct Smem {
   double scale, invsig_tmp;
   int k;
   int flag;
+  int sweeps;
+  int rotcount;
+  unsigned long long* prof;
   int sample;
   int center;
 };
@@ -217,10 +225,32 @@ __device__ int hestenes(double2* W, int Mw, int Nw, Smem& sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Np = Nw + (Nw & 1);
   if (Nw < 2) return 0;
-  const double tol = sqrt((double)Mw) * 1.1102230246251565e-16;
+  // off-diagonal threshold ~2 eps sqrt(M): above the rounding noise of a
+  // length-M complex dot product, so converged pairs do not re-trigger
+  const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16;
   int sweep = 0;
   for (; sweep < MAXSWEEP; ++sweep) {
-    if (threadIdx.x == 0) sm.flag = 0;
+    // numerically dead columns (|a|^2 < 1e-28 |A|_F^2, i.e. rounding residue of
+    // a rank deficiency) are set exactly to zero; they can never be made
+    // orthogonal to the live span and would otherwise rotate forever
+    for (int c = warp; c < Nw; c += NWARP) {
+      double s = 0.0;
+      for (int y = lane; y < Mw; y += 32) s += abs2(W[(size_t)c * Mw + y]);
+      s = warp_sum(s);
+      if (lane == 0) sm.sig[c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int c = 0; c < Nw; ++c) t += sm.sig[c];
+      sm.scale = t;
+      sm.flag = 0;
+    }
+    __syncthreads();
+    const double dead = 1e-28 * sm.scale;
+    for (int c = warp; c < Nw; c += NWARP)
+      if (sm.sig[c] < dead && sm.sig[c] > 0.0)
+        for (int y = lane; y < Mw; y += 32) W[(size_t)c * Mw + y] = cz();
     __syncthreads();
     for (int r = 0; r < Np - 1; ++r) {
       for (int p = warp; p < Np / 2; p += NWARP) {
@@ -301,8 +331,523 @@ __device__ void sort_sigma(const double2* W, int Mw, int Nw, Smem& sm) {
 }
 
 // ----------------------------------------------------------------------------
+// Shared-memory resident one-sided Jacobi (Mw <= 128, Nw <= 128).
+//
+// Columns live in blocks of 32: three shared-memory slots (A, B, C) and, when
+// Nw > 96, one L2 slot G (global W columns 96..127).  RPL = rows per lane.
+// A sweep visits every column pair exactly once:
+//   within A, B, C (round robin, columns streamed from smem)
+//   G x {A, B, C}  (G held in registers, 2 columns per warp, A/B/C streamed)
+//   swap contents of A and G; within A
+//   G x {B, C};  B x C
+// Every warp step processes two independent pairs so one transposed warp
+// reduction and one half-warp parameter evaluation serve both.
+// ----------------------------------------------------------------------------
+constexpr int JB = 32;  // columns per block
+
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts2(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
+template <int RPL>
+struct Col {
+  double2 v[RPL];
+};
+
+// smem column at byte address a (lane-strided rows)
+template <int RPL>
+__device__ __forceinline__ void col_lds(Col<RPL>& c, uint32_t a) {
+  const uint32_t l = (threadIdx.x & 31) * 16u;
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) c.v[q] = lds2(a + l + 512u * q);
+}
+template <int RPL>
+__device__ __forceinline__ void col_sts(uint32_t a, const Col<RPL>& c) {
+  const uint32_t l = (threadIdx.x & 31) * 16u;
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) sts2(a + l + 512u * q, c.v[q]);
+}
+template <int RPL>
+__device__ __forceinline__ void col_load_g(Col<RPL>& c, const double2* p, int Mw) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) {
+    const int y = lane + 32 * q;
+    c.v[q] = (y < Mw) ? p[y] : cz();
+  }
+}
+template <int RPL>
+__device__ __forceinline__ void col_store_g(double2* p, const Col<RPL>& c, int Mw) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) {
+    const int y = lane + 32 * q;
+    if (y < Mw) p[y] = c.v[q];
+  }
+}
+
+// Rotation of one pair.  Identity when s == 0 (c = 1, e = 1).
+struct Rot {
+  double c, s, er, ei, tg;
+};
+
+// Jacobi parameters for one pair (alpha = |a|^2, beta = |b|^2, g = a^H b):
+// t = 2|g| sgn(d) / (|d| + sqrt(d^2 + 4|g|^2)), d = beta - alpha (the smaller
+// root of t^2 + 2 zeta t - 1 = 0), c = 1/sqrt(1+t^2), s = t c, e = conj(g)/|g|.
+// A pair is left alone when it is orthogonal to relative precision
+// (|g|^2 <= tol2 alpha beta) or when the rotation would move either column by
+// less than the absolute rounding floor of the matrix (|g|^2 <= abs2 *
+// max(alpha, beta)) — the same absolute accuracy LAPACK's SVD delivers.
+__device__ __forceinline__ Rot rot_params(double gr, double gi, double al, double be, bool valid, double tol2,
+                                          double abs2) {
+  Rot p;
+  const double g2 = fma(gr, gr, gi * gi);
+  const bool rot = valid && (g2 > tol2 * al * be) && (g2 > abs2 * fmax(al, be));
+  p.c = 1.0;
+  p.s = 0.0;
+  p.er = 1.0;
+  p.ei = 0.0;
+  p.tg = 0.0;
+  if (rot) {
+    const double ig = rsqrt(g2);
+    const double g = g2 * ig;
+    const double d = be - al;
+    const double den = fabs(d) + sqrt(fma(d, d, 4.0 * g2));
+    const double t = copysign(2.0 * g, d) / den;
+    p.c = rsqrt(fma(t, t, 1.0));
+    p.s = t * p.c;
+    p.er = gr * ig;
+    p.ei = -gi * ig;
+    p.tg = t * g;
+  }
+  return p;
+}
+
+__device__ __forceinline__ Rot shfl_rot(const Rot& p, int src) {
+  Rot o;
+  o.c = __shfl_sync(0xffffffffu, p.c, src);
+  o.s = __shfl_sync(0xffffffffu, p.s, src);
+  o.er = __shfl_sync(0xffffffffu, p.er, src);
+  o.ei = __shfl_sync(0xffffffffu, p.ei, src);
+  o.tg = __shfl_sync(0xffffffffu, p.tg, src);
+  return o;
+}
+
+// a' = c a - s e b,  b' = s a + c e b
+template <int RPL>
+__device__ __forceinline__ void apply_rot(Col<RPL>& a, Col<RPL>& b, const Rot& p) {
+  const double sre = p.s * p.er, sim = p.s * p.ei, cre = p.c * p.er, cim = p.c * p.ei;
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) {
+    const double2 x = a.v[q], y = b.v[q];
+    double2 na, nb;
+    na.x = fma(sim, y.y, fma(-sre, y.x, p.c * x.x));
+    na.y = fma(-sim, y.x, fma(-sre, y.y, p.c * x.y));
+    nb.x = fma(-cim, y.y, fma(cre, y.x, p.s * x.x));
+    nb.y = fma(cim, y.x, fma(cre, y.y, p.s * x.y));
+    a.v[q] = na;
+    b.v[q] = nb;
+  }
+}
+
+struct Thr {
+  double tol2, abs2;
+};
+
+// two independent pairs (a0,b0), (a1,b1); returns true if any rotation applied
+template <int RPL>
+__device__ __forceinline__ bool rot2(Col<RPL>& a0, Col<RPL>& b0, double& na0, double& nb0, bool v0, Col<RPL>& a1,
+                                     Col<RPL>& b1, double& na1, double& nb1, bool v1, const Thr& th) {
+  const int lane = threadIdx.x & 31;
+  double2 g0 = cz(), g1 = cz();
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) {
+    cfmac(g0, a0.v[q], b0.v[q]);
+    cfmac(g1, a1.v[q], b1.v[q]);
+  }
+  // transposed reduction of (g0.x, g0.y, g1.x, g1.y): lanes 0-15 end with g0,
+  // lanes 16-31 with g1
+  const bool up = lane & 16;
+  double x0 = up ? g1.x : g0.x, x1 = up ? g1.y : g0.y;
+  const double y0 = up ? g0.x : g1.x, y1 = up ? g0.y : g1.y;
+  x0 += __shfl_xor_sync(0xffffffffu, y0, 16);
+  x1 += __shfl_xor_sync(0xffffffffu, y1, 16);
+  const bool h8 = lane & 8;
+  double z = h8 ? x1 : x0;
+  const double w = h8 ? x0 : x1;
+  z += __shfl_xor_sync(0xffffffffu, w, 8);
+  z += __shfl_xor_sync(0xffffffffu, z, 4);
+  z += __shfl_xor_sync(0xffffffffu, z, 2);
+  z += __shfl_xor_sync(0xffffffffu, z, 1);
+  const double o = __shfl_xor_sync(0xffffffffu, z, 8);
+  const double gr = h8 ? o : z, gi = h8 ? z : o;
+  const Rot mine = rot_params(gr, gi, up ? na1 : na0, up ? nb1 : nb0, up ? v1 : v0, th.tol2, th.abs2);
+  const Rot p0 = shfl_rot(mine, 0), p1 = shfl_rot(mine, 16);
+  const bool r0 = p0.s != 0.0, r1 = p1.s != 0.0;
+  if (r0) apply_rot(a0, b0, p0);
+  if (r1) apply_rot(a1, b1, p1);
+  // tracked norms; a relative drop below 1/2 means cancellation, so those
+  // columns get their exact norm (warp-uniform branch, rare after sweep 1)
+  const double na0n = na0 - p0.tg, nb0n = nb0 + p0.tg, na1n = na1 - p1.tg, nb1n = nb1 + p1.tg;
+  const bool f0 = r0 && na0n < 0.5 * na0, f1 = r0 && nb0n < 0.5 * nb0;
+  const bool f2 = r1 && na1n < 0.5 * na1, f3 = r1 && nb1n < 0.5 * nb1;
+  na0 = na0n;
+  nb0 = nb0n;
+  na1 = na1n;
+  nb1 = nb1n;
+  if (f0 || f1 || f2 || f3) {
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      e0 += abs2(a0.v[q]);
+      e1 += abs2(b0.v[q]);
+      e2 += abs2(a1.v[q]);
+      e3 += abs2(b1.v[q]);
+    }
+    if (f0) na0 = warp_sum(e0);
+    if (f1) nb0 = warp_sum(e1);
+    if (f2) na1 = warp_sum(e2);
+    if (f3) nb1 = warp_sum(e3);
+  }
+  return r0 || r1;
+}
+
+template <int RPL>
+struct JacobiSmem {
+  static constexpr int LD = 32 * RPL;  // padded rows per smem column
+  static constexpr uint32_t CB = LD * 16u;  // bytes per smem column
+  uint32_t base;                       // smem byte address of slot A
+  double2* sp;                         // generic pointer to slot A (staging only)
+  double2* G;                          // global columns 96..127 (ld = Mw)
+  int Mw, nblk;
+  int ncol[4];                         // live columns per slot (A, B, C, G)
+  Thr th;
+
+  __device__ uint32_t scol(int s, int c) const { return base + (uint32_t)(s * JB + c) * CB; }
+
+  // within-block round robin on up to three smem slots concurrently
+  __device__ void within(const int* slots, int ns, Smem& sm) {
+    const int warp = threadIdx.x >> 5;
+    int rounds = 0;
+    for (int x = 0; x < ns; ++x) {
+      const int nb = ncol[slots[x]];
+      rounds = max(rounds, nb + (nb & 1) - 1);
+    }
+    for (int r = 0; r < rounds; ++r) {
+      bool any = false;
+      int cnt = 0;
+      int ps0 = 0, is0 = 0, js0 = 0, ps1 = 0, is1 = 0, js1 = 0, ps2 = 0, is2 = 0, js2 = 0;
+      for (int x = 0; x < ns; ++x) {
+        const int s = slots[x], nb = ncol[s], nbp = nb + (nb & 1);
+        if (r < nbp - 1 && warp < nbp / 2) {
+          int i, j;
+          rr_pair(r, warp, nbp, i, j);
+          if (i < nb && j < nb) {
+            if (cnt == 0) { ps0 = s; is0 = i; js0 = j; }
+            else if (cnt == 1) { ps1 = s; is1 = i; js1 = j; }
+            else { ps2 = s; is2 = i; js2 = j; }
+            ++cnt;
+          }
+        }
+      }
+      for (int k = 0; k < cnt; k += 2) {
+        const bool two = (k + 1 < cnt);
+        const int pa = k ? ps2 : ps0, ia = k ? is2 : is0, ja = k ? js2 : js0;
+        Col<RPL> a0, b0, a1, b1;
+        col_lds(a0, scol(pa, ia));
+        col_lds(b0, scol(pa, ja));
+        double na0 = sm.nrm[pa * JB + ia], nb0 = sm.nrm[pa * JB + ja];
+        double na1 = 0.0, nb1 = 0.0;
+        if (two) {
+          col_lds(a1, scol(ps1, is1));
+          col_lds(b1, scol(ps1, js1));
+          na1 = sm.nrm[ps1 * JB + is1];
+          nb1 = sm.nrm[ps1 * JB + js1];
+        } else {
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) a1.v[q] = b1.v[q] = cz();
+        }
+        const bool rr = rot2<RPL>(a0, b0, na0, nb0, true, a1, b1, na1, nb1, two, th);
+        if (rr && (threadIdx.x & 31) == 0) atomicAdd(&sm.rotcount, 1);
+        if (rr) {
+          any = true;
+          col_sts(scol(pa, ia), a0);
+          col_sts(scol(pa, ja), b0);
+          if (two) {
+            col_sts(scol(ps1, is1), a1);
+            col_sts(scol(ps1, js1), b1);
+          }
+          if ((threadIdx.x & 31) == 0) {
+            sm.nrm[pa * JB + ia] = na0;
+            sm.nrm[pa * JB + ja] = nb0;
+            if (two) {
+              sm.nrm[ps1 * JB + is1] = na1;
+              sm.nrm[ps1 * JB + js1] = nb1;
+            }
+          }
+        }
+      }
+      if (any && (threadIdx.x & 31) == 0) sm.flag = 1;
+      __syncthreads();
+    }
+  }
+
+  // P (registers: columns 2w, 2w+1) against smem slot sq
+  __device__ void cross(Col<RPL>& p0, Col<RPL>& p1, double& np0, double& np1, int nP, int sq, Smem& sm) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nQ = ncol[sq];
+    const bool vp0 = 2 * warp < nP, vp1 = 2 * warp + 1 < nP;
+    bool any = false;
+    for (int r = 0; r < 16; ++r) {
+      const int g = (warp + r) & 15;
+      const bool vq0 = 2 * g < nQ, vq1 = 2 * g + 1 < nQ;
+      if ((vp0 || vp1) && (vq0 || vq1)) {
+        Col<RPL> q0, q1;
+        const uint32_t a0 = scol(sq, 2 * g), a1 = scol(sq, 2 * g + 1);
+        col_lds(q0, a0);
+        col_lds(q1, a1);
+        double nq0 = sm.nrm[sq * JB + 2 * g], nq1 = sm.nrm[sq * JB + 2 * g + 1];
+        bool rr = rot2<RPL>(p0, q0, np0, nq0, vp0 && vq0, p1, q1, np1, nq1, vp1 && vq1, th);
+        const bool rr2 = rot2<RPL>(p0, q1, np0, nq1, vp0 && vq1, p1, q0, np1, nq0, vp1 && vq0, th);
+        if (lane == 0 && (rr || rr2)) atomicAdd(&sm.rotcount, (int)rr + (int)rr2);
+        rr |= rr2;
+        if (rr) {
+          any = true;
+          col_sts(a0, q0);
+          col_sts(a1, q1);
+          if (lane == 0) {
+            sm.nrm[sq * JB + 2 * g] = nq0;
+            sm.nrm[sq * JB + 2 * g + 1] = nq1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (any && lane == 0) sm.flag = 1;
+  }
+
+  __device__ void load_p_smem(Col<RPL>& p0, Col<RPL>& p1, double& n0, double& n1, int s, Smem& sm) {
+    const int warp = threadIdx.x >> 5;
+    col_lds(p0, scol(s, 2 * warp));
+    col_lds(p1, scol(s, 2 * warp + 1));
+    n0 = sm.nrm[s * JB + 2 * warp];
+    n1 = sm.nrm[s * JB + 2 * warp + 1];
+  }
+  __device__ void store_p_smem(const Col<RPL>& p0, const Col<RPL>& p1, double n0, double n1, int s, Smem& sm) {
+    const int warp = threadIdx.x >> 5;
+    col_sts(scol(s, 2 * warp), p0);
+    col_sts(scol(s, 2 * warp + 1), p1);
+    if ((threadIdx.x & 31) == 0) {
+      sm.nrm[s * JB + 2 * warp] = n0;
+      sm.nrm[s * JB + 2 * warp + 1] = n1;
+    }
+  }
+  __device__ void load_p_g(Col<RPL>& p0, Col<RPL>& p1, double& n0, double& n1, Smem& sm) {
+    const int warp = threadIdx.x >> 5;
+    col_load_g(p0, G + (size_t)(2 * warp) * Mw, Mw);
+    col_load_g(p1, G + (size_t)(2 * warp + 1) * Mw, Mw);
+    n0 = sm.nrm[3 * JB + 2 * warp];
+    n1 = sm.nrm[3 * JB + 2 * warp + 1];
+  }
+  __device__ void store_p_g(const Col<RPL>& p0, const Col<RPL>& p1, double n0, double n1, Smem& sm) {
+    const int warp = threadIdx.x >> 5;
+    col_store_g(G + (size_t)(2 * warp) * Mw, p0, Mw);
+    col_store_g(G + (size_t)(2 * warp + 1) * Mw, p1, Mw);
+    if ((threadIdx.x & 31) == 0) {
+      sm.nrm[3 * JB + 2 * warp] = n0;
+      sm.nrm[3 * JB + 2 * warp + 1] = n1;
+    }
+  }
+
+  // exact norms of every column; zero the numerically dead ones; thresholds
+  __device__ void refresh_norms(Smem& sm, double tol) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < JB * nblk; c += NWARP) {
+      const int s = c / JB, k = c - s * JB;
+      double acc = 0.0;
+      if (s < 3) {
+        Col<RPL> v;
+        col_lds(v, scol(s, k));
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) acc += abs2(v.v[q]);
+      } else {
+        const double2* p = G + (size_t)k * Mw;
+        for (int y = lane; y < Mw; y += 32) acc += abs2(p[y]);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) sm.nrm[c] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0, mx = 0.0;
+      for (int c = 0; c < JB * nblk; ++c) {
+        t += sm.nrm[c];
+        mx = fmax(mx, sm.nrm[c]);
+      }
+      sm.scale = t;
+      sm.invsig_tmp = mx;
+      sm.flag = 0;
+    }
+    __syncthreads();
+    th.tol2 = tol * tol;
+    th.abs2 = 0.0;  // relative criterion only: the split projects onto Q, which must be orthonormal
+    const double dead = 1e-28 * sm.scale;
+    for (int c = warp; c < JB * nblk; c += NWARP) {
+      const double v = sm.nrm[c];
+      if (v < dead && v > 0.0) {
+        const int s = c / JB, k = c - s * JB;
+        if (s < 3) {
+          Col<RPL> z;
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) z.v[q] = cz();
+          col_sts(scol(s, k), z);
+        } else {
+          double2* p = G + (size_t)k * Mw;
+          for (int y = lane; y < Mw; y += 32) p[y] = cz();
+        }
+        if (lane == 0) sm.nrm[c] = 0.0;
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ void sweep(Smem& sm) {
+    const int all3[3] = {0, 1, 2};
+    const int nsm = min(nblk, 3);
+    within(all3, nsm, sm);
+    if (nblk == 4) {
+      {
+        Col<RPL> p0, p1;
+        double n0, n1;
+        load_p_g(p0, p1, n0, n1, sm);
+        for (int s = 0; s < 3; ++s) cross(p0, p1, n0, n1, ncol[3], s, sm);
+        // swap contents: A -> G storage, P (old G) -> A
+        Col<RPL> t0, t1;
+        double m0, m1;
+        load_p_smem(t0, t1, m0, m1, 0, sm);
+        __syncthreads();
+        store_p_smem(p0, p1, n0, n1, 0, sm);
+        store_p_g(t0, t1, m0, m1, sm);
+        const int na = ncol[0];
+        ncol[0] = ncol[3];
+        ncol[3] = na;
+        __syncthreads();
+      }
+      const int a1[1] = {0};
+      within(a1, 1, sm);
+      {
+        Col<RPL> p0, p1;
+        double n0, n1;
+        load_p_g(p0, p1, n0, n1, sm);
+        cross(p0, p1, n0, n1, ncol[3], 1, sm);
+        cross(p0, p1, n0, n1, ncol[3], 2, sm);
+        store_p_g(p0, p1, n0, n1, sm);
+        __syncthreads();
+      }
+      {
+        Col<RPL> p0, p1;
+        double n0, n1;
+        load_p_smem(p0, p1, n0, n1, 1, sm);
+        cross(p0, p1, n0, n1, ncol[1], 2, sm);
+        store_p_smem(p0, p1, n0, n1, 1, sm);
+        __syncthreads();
+      }
+    } else {
+      for (int sp = 0; sp + 1 < nsm; ++sp) {
+        Col<RPL> p0, p1;
+        double n0, n1;
+        load_p_smem(p0, p1, n0, n1, sp, sm);
+        for (int sq = sp + 1; sq < nsm; ++sq) cross(p0, p1, n0, n1, ncol[sp], sq, sm);
+        store_p_smem(p0, p1, n0, n1, sp, sm);
+        __syncthreads();
+      }
+    }
+  }
+};
+
+// Runs the smem Jacobi on W (global, Mw x Nw col-major); on return W holds
+// the rotated columns in positions [0, Nw_eff); returns Nw_eff, negated on
+// non-convergence after MAXSWEEP sweeps.
+template <int RPL>
+__device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) {
+  JacobiSmem<RPL> J;
+  constexpr int LD = JacobiSmem<RPL>::LD;
+  J.Mw = Mw;
+  J.nblk = (Nw + JB - 1) / JB;
+  J.base = (uint32_t)__cvta_generic_to_shared(smem);
+  J.sp = smem;
+  J.G = W + (size_t)3 * JB * Mw;
+  for (int b = 0; b < 4; ++b) J.ncol[b] = max(0, min(JB, Nw - JB * b));
+  const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16;
+  // stage W into the smem slots (zero padding), zero the unused G columns
+  const int nsm = min(J.nblk, 3);
+  for (int e = threadIdx.x; e < nsm * JB * LD; e += NT) {
+    const int c = e / LD, y = e - c * LD;
+    smem[e] = (c < Nw && y < Mw) ? W[(size_t)c * Mw + y] : cz();
+  }
+  if (J.nblk == 4)
+    for (int e = threadIdx.x; e < JB * Mw; e += NT) {
+      const int k = e / Mw;
+      if (3 * JB + k >= Nw) J.G[e] = cz();
+    }
+  __syncthreads();
+  int sweep = 0;
+  bool conv = false;
+  for (; sweep < MAXSWEEP; ++sweep) {
+    if (threadIdx.x == 0) sm.rotcount = 0;
+    J.refresh_norms(sm, tol);
+    J.sweep(sm);
+    __syncthreads();
+    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[16 + min(sweep, 47)], (unsigned long long)sm.rotcount);
+    if (sm.flag == 0) {
+      conv = true;
+      break;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sm.sweeps = sweep + 1;
+  // write the smem slots back to W columns [0, 32*nsm)
+  for (int e = threadIdx.x; e < nsm * JB * Mw; e += NT) {
+    const int c = e / Mw, y = e - c * Mw;
+    W[(size_t)c * Mw + y] = smem[(size_t)c * LD + y];
+  }
+  __syncthreads();
+  const int neff = (J.nblk == 1) ? Nw : JB * J.nblk;
+  return conv ? neff : -neff;
+}
+
+// dispatcher: returns the number of (possibly padded) result columns in W;
+// sets status bit 0 on non-convergence
+__device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
+  int neff;
+  if (Nw < 2) return Nw;
+  if (Mw <= 32 && Nw <= 128) neff = jacobi_smem<1>(W, Mw, Nw, sm, smem);
+  else if (Mw <= 64 && Nw <= 128) neff = jacobi_smem<2>(W, Mw, Nw, sm, smem);
+  else if (Mw <= 128 && Nw <= 128) neff = jacobi_smem<4>(W, Mw, Nw, sm, smem);
+  else {
+    const int sw = hestenes(W, Mw, Nw, sm);
+    neff = (sw > MAXSWEEP) ? -Nw : Nw;
+  }
+  if (neff < 0) {
+    if (threadIdx.x == 0) atomicOr(status, 1);
+    neff = -neff;
+  }
+  return neff;
+}
+
+// ----------------------------------------------------------------------------
 // Per-CTA sample context
 // ----------------------------------------------------------------------------
+__device__ __forceinline__ long long prof_clock() { return clock64(); }
+__device__ __forceinline__ void prof_add(const Job& jb, int slot, long long v) {
+  if (threadIdx.x == 0 && jb.prof) atomicAdd(&jb.prof[slot], (unsigned long long)v);
+}
+
 struct Ctx {
   const Job* job;
   double2* mps;
@@ -329,6 +874,7 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   double2* B = cx.site(s + 1);
   double2* W = cx.W;
   double2* W0 = cx.W0;
+  const long long t0 = prof_clock();
 
   // theta = A (2cl x cm) . B (cm x 2cr), written into W in the Jacobi orientation
   cta_gemm<true, false>(
@@ -394,9 +940,20 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   }
   __syncthreads();
 
-  const int sweeps = hestenes(W, Mw, Nw, sm);
-  if (sweeps > MAXSWEEP && threadIdx.x == 0) atomicOr(jb.status, 1);
-  sort_sigma(W, Mw, Nw, sm);
+  const long long t1 = prof_clock();
+  if (threadIdx.x == 0) sm.sweeps = 0;
+  const int Neff = jacobi(W, Mw, Nw, sm, cx.tile, jb.status);
+  const long long t2 = prof_clock();
+  prof_add(jb, 4, t1 - t0);
+  prof_add(jb, 0, t2 - t1);
+  prof_add(jb, 1, 1);
+  prof_add(jb, 2, sm.sweeps);
+  if (Mw == 128 && Nw == 128) {
+    prof_add(jb, 9, t2 - t1);
+    prof_add(jb, 10, 1);
+    prof_add(jb, 11, sm.sweeps);
+  }
+  sort_sigma(W, Mw, Neff, sm);
 
   // truncation rule + renormalisation (_kernel.py:118-131)
   if (threadIdx.x == 0) {
@@ -458,6 +1015,7 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
       cx.tile);
   if (threadIdx.x == 0) sm.dims[s + 1] = k;
   __syncthreads();
+  prof_add(jb, 5, prof_clock() - t2);
 }
 
 // ----------------------------------------------------------------------------
@@ -592,6 +1150,8 @@ __device__ void move_left(const Ctx& cx, Smem& sm, int c) {
 }
 
 __device__ void ensure_center(const Ctx& cx, Smem& sm, int s) {
+  const long long t0 = prof_clock();
+  const bool moved = sm.center < s || sm.center > s + 1;
   while (sm.center < s) {
     move_right(cx, sm, sm.center);
     if (threadIdx.x == 0) sm.center += 1;
@@ -602,6 +1162,7 @@ __device__ void ensure_center(const Ctx& cx, Smem& sm, int s) {
     if (threadIdx.x == 0) sm.center -= 1;
     __syncthreads();
   }
+  if (moved) prof_add(*cx.job, 3, prof_clock() - t0);
 }
 
 // one-site rotation exp(-i angle/2 P) (_kernel.py:105-111); with pauli=true
@@ -753,7 +1314,9 @@ __device__ void measure_z(const Ctx& cx, Smem& sm) {
 
 __device__ void record_checkpoint(const Ctx& cx, Smem& sm, int sample, int ck) {
   const Job& jb = *cx.job;
+  const long long t0 = prof_clock();
   measure_z(cx, sm);
+  prof_add(jb, 6, prof_clock() - t0);
   const double sign = jb.ckpt_sign ? (double)jb.ckpt_sign[(size_t)sample * jb.n_ckpt + ck] : 1.0;
   for (int o = threadIdx.x; o < jb.n_obs; o += NT) {
     const double z = sm.zval[jb.obs_sites[o]];
@@ -761,8 +1324,9 @@ __device__ void record_checkpoint(const Ctx& cx, Smem& sm, int sample, int ck) {
     const double v = sign * z;
     const long long qv = llrint(v * FIX);
     const long long qv2 = llrint(z * z * FIX);
-    atomicAdd(&jb.sum_v[(size_t)ck * jb.n_obs + o], (unsigned long long)qv);
-    atomicAdd(&jb.sum_v2[(size_t)ck * jb.n_obs + o], (unsigned long long)qv2);
+    const size_t row = jb.sum_row ? (size_t)jb.sum_row[(size_t)sample * jb.n_ckpt + ck] : (size_t)ck;
+    atomicAdd(&jb.sum_v[row * jb.n_obs + o], (unsigned long long)qv);
+    atomicAdd(&jb.sum_v2[row * jb.n_obs + o], (unsigned long long)qv2);
   }
   if (threadIdx.x == 0 && jb.discarded) jb.discarded[(size_t)sample * jb.n_ckpt + ck] = sm.counters[3];
   __syncthreads();
@@ -783,14 +1347,24 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
   cx.W0 = job.ws_W0 + job.mat_stride * blockIdx.x;
   cx.X = job.ws_X + job.mat_stride * blockIdx.x;
   cx.tile = dyn_smem;
-  if (threadIdx.x == 0) sm.flops = 0.0;
-  for (;;) {
-    if (threadIdx.x == 0) sm.sample = atomicAdd(job.next_sample, 1);
+  if (threadIdx.x == 0) {
+    sm.flops = 0.0;
+    sm.prof = job.prof;
+  }
+  for (int iter = 0;; ++iter) {
+    if (job.slot_mode) {
+      if (iter > 0 || (int)blockIdx.x >= job.n_samples) break;
+      if (threadIdx.x == 0) sm.sample = blockIdx.x;
+    } else if (threadIdx.x == 0) {
+      sm.sample = atomicAdd(job.next_sample, 1);
+    }
     __syncthreads();
     const int sample = sm.sample;
     if (sample >= job.n_samples) break;
-    // --- initial state
-    if (job.init_vecs) {
+    int* sdims = job.slot_dims + (size_t)blockIdx.x * (MAXN + 1);
+    // --- initial state: product state, or the slot's persistent state
+    const bool fresh = !job.slot_mode || (job.reset && job.reset[sample]);
+    if (fresh) {
       for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = 1;
       for (int e = threadIdx.x; e < n * 2; e += NT) {
         const int s = e >> 1, i = e & 1;
@@ -802,13 +1376,14 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
         sm.counters[2] = 1.0;
       }
     } else {
-      for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = job.io_dims[e];
+      for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = sdims[e];
       if (threadIdx.x == 0) {
-        sm.center = *job.io_center;
-        for (int q = 0; q < 4; ++q) sm.counters[q] = job.io_counters[q];
+        sm.center = job.slot_center[blockIdx.x];
+        for (int q = 0; q < 4; ++q) sm.counters[q] = job.slot_counters[(size_t)blockIdx.x * 4 + q];
       }
     }
     __syncthreads();
+    const long long tstart = prof_clock();
     const int64_t g0 = job.gate_off[sample], g1 = job.gate_off[sample + 1];
     int ck = 0;
     for (int64_t gi = g0; gi < g1; ++gi) {
@@ -856,16 +1431,17 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
       record_checkpoint(cx, sm, sample, ck);
       ++ck;
     }
+    prof_add(job, 7, prof_clock() - tstart);
     if (threadIdx.x == 0) {
       if (job.ledger)
         for (int q = 0; q < 4; ++q) job.ledger[(size_t)sample * 4 + q] = sm.counters[q];
-      if (!job.init_vecs) {
-        *job.io_center = sm.center;
-        for (int q = 0; q < 4; ++q) job.io_counters[q] = sm.counters[q];
+      if (job.slot_mode) {
+        job.slot_center[blockIdx.x] = sm.center;
+        for (int q = 0; q < 4; ++q) job.slot_counters[(size_t)blockIdx.x * 4 + q] = sm.counters[q];
       }
     }
-    if (!job.init_vecs)
-      for (int e = threadIdx.x; e < n + 1; e += NT) job.io_dims[e] = sm.dims[e];
+    if (job.slot_mode)
+      for (int e = threadIdx.x; e < n + 1; e += NT) sdims[e] = sm.dims[e];
     __syncthreads();
   }
   if (threadIdx.x == 0) job.flops[blockIdx.x] += sm.flops;
@@ -925,9 +1501,10 @@ __global__ void __launch_bounds__(NT, 1) expectation_kernel(const double2* buf, 
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int n, double2* Wg, double2* W0g,
                                                     size_t mat_stride, double* s, double2* u, double2* vh,
-                                                    int* status) {
+                                                    int* status, unsigned long long* prof) {
   extern __shared__ double2 dyn_smem[];
   __shared__ Smem sm;
+  if (threadIdx.x == 0) sm.prof = prof;
   const int b = blockIdx.x;
   const int K = min(m, n);
   double2* W = Wg + mat_stride * b;
@@ -940,9 +1517,12 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
     W0[(size_t)c * m + y] = A[e];
   }
   __syncthreads();
-  const int sweeps = hestenes(W, m, n, sm);
-  if (sweeps > MAXSWEEP && threadIdx.x == 0) atomicOr(status, 1);
-  sort_sigma(W, m, n, sm);
+  const int Neff = jacobi(W, m, n, sm, dyn_smem, status);
+  if (threadIdx.x == 0 && prof) {
+    atomicAdd(&prof[1], 1ull);
+    atomicAdd(&prof[2], (unsigned long long)sm.sweeps);
+  }
+  sort_sigma(W, m, Neff, sm);
   for (int i = threadIdx.x; i < K; i += NT) s[(size_t)b * K + i] = sm.sig[sm.perm[i]];
   if (u)
     for (int e = threadIdx.x; e < m * K; e += NT) {
@@ -964,6 +1544,8 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
 }
 
 constexpr size_t kTileBytes = 2 * TK * TLD * sizeof(double2);
+constexpr size_t kDynSmem = 3 * JB * 128 * sizeof(double2);  // >= kTileBytes (aliased)
+static_assert(kDynSmem >= kTileBytes, "tile buffer aliases the Jacobi slots");
 
 __global__ void sum_flops_kernel(const double* f, int n, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -982,18 +1564,22 @@ struct tb_ctx {
   int device = 0;
   int sms = 0;
   std::string err;
-  // workspace
+  // per-slot workspace (one slot per persistent CTA)
   double2* mps = nullptr;
   double2* W = nullptr;
   double2* W0 = nullptr;
   double2* X = nullptr;
+  int* slot_dims = nullptr;
+  int* slot_center = nullptr;
+  double* slot_counters = nullptr;
   size_t mps_cap_bytes = 0, mat_cap_bytes = 0;  // per slot
   int slots = 0;
   size_t mps_stride = 0, mat_stride = 0;
+  int state_n = -1, state_cap = -1;  // shape the slot states were built for
   // small device scratch
-  int* dscratch = nullptr;  // [0] next_sample, [1] status, [2] center, [3..] dims
+  int* dscratch = nullptr;  // [0] next_sample, [1] status
   double* dflops = nullptr;
-  double* dcounters = nullptr;
+  unsigned long long* dprof = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
@@ -1004,300 +1590,80 @@ int fail(tb_ctx* c, int code, const std::string& msg) {
   return code;
 }
 
-#define TB_CUDA(ctx, call)                                                                      \
-  do {                                                                                          \
-    cudaError_t _e = (call);                                                                    \
+#define TB_CUDA(ctx, call)                                                                               \
+  do {                                                                                                   \
+    cudaError_t _e = (call);                                                                             \
     if (_e != cudaSuccess) return fail(ctx, TB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
-int ensure_workspace(tb_ctx* c, int slots, int n, int cap) {
-  const size_t mps_bytes = (size_t)n * cap * 2 * cap * sizeof(double2);
-  const size_t mat_bytes = (size_t)(2 * cap) * (2 * cap) * sizeof(double2);
-  if (slots <= c->slots && mps_bytes <= c->mps_cap_bytes && mat_bytes <= c->mat_cap_bytes) {
-    c->mps_stride = mps_bytes / sizeof(double2);
-    c->mat_stride = mat_bytes / sizeof(double2);
-    return TB_OK;
-  }
+void free_workspace(tb_ctx* c) {
   cudaFree(c->mps);
   cudaFree(c->W);
   cudaFree(c->W0);
   cudaFree(c->X);
+  cudaFree(c->slot_dims);
+  cudaFree(c->slot_center);
+  cudaFree(c->slot_counters);
   c->mps = c->W = c->W0 = c->X = nullptr;
+  c->slot_dims = c->slot_center = nullptr;
+  c->slot_counters = nullptr;
+  c->slots = 0;
+  c->mps_cap_bytes = c->mat_cap_bytes = 0;
+  c->state_n = c->state_cap = -1;
+}
+
+// Grow the per-slot workspace to `slots` slots of an (n, cap) chain.  Slot
+// states survive only while the shape is unchanged and nothing is reallocated.
+int ensure_workspace(tb_ctx* c, int slots, int n, int cap) {
+  const size_t mps_bytes = (size_t)n * cap * 2 * cap * sizeof(double2);
+  const size_t cols = (size_t)((2 * cap + 31) / 32) * 32;
+  const size_t mat_bytes = (size_t)(2 * cap) * (cols > (size_t)(2 * cap) ? cols : (size_t)(2 * cap)) * sizeof(double2);
+  c->mps_stride = mps_bytes / sizeof(double2);
+  c->mat_stride = mat_bytes / sizeof(double2);
+  if (slots <= c->slots && mps_bytes <= c->mps_cap_bytes && mat_bytes <= c->mat_cap_bytes) {
+    if (n != c->state_n || cap != c->state_cap) c->state_n = c->state_cap = -1;
+    return TB_OK;
+  }
   const int s = slots > c->slots ? slots : c->slots;
   const size_t mb = mps_bytes > c->mps_cap_bytes ? mps_bytes : c->mps_cap_bytes;
   const size_t tb = mat_bytes > c->mat_cap_bytes ? mat_bytes : c->mat_cap_bytes;
+  free_workspace(c);
   if (cudaMalloc(&c->mps, mb * s) != cudaSuccess || cudaMalloc(&c->W, tb * s) != cudaSuccess ||
-      cudaMalloc(&c->W0, tb * s) != cudaSuccess || cudaMalloc(&c->X, tb * s) != cudaSuccess) {
+      cudaMalloc(&c->W0, tb * s) != cudaSuccess || cudaMalloc(&c->X, tb * s) != cudaSuccess ||
+      cudaMalloc(&c->slot_dims, (size_t)s * (tb::MAXN + 1) * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->slot_center, (size_t)s * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->slot_counters, (size_t)s * 4 * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
-    c->slots = 0;
-    c->mps_cap_bytes = c->mat_cap_bytes = 0;
+    free_workspace(c);
     return fail(c, TB_ENOMEM, "workspace allocation failed");
   }
   c->slots = s;
   c->mps_cap_bytes = mb;
   c->mat_cap_bytes = tb;
-  c->mps_stride = mps_bytes / sizeof(double2);
-  c->mat_stride = mat_bytes / sizeof(double2);
   return TB_OK;
 }
 
 int validate_shape(tb_ctx* c, int64_t n, int64_t cap, int64_t chi_cut) {
   if (n < 1 || n > tb::MAXN) return fail(c, TB_EINVAL, "n must lie in [1, 64]");
   if (cap < 1 || cap > tb::MAXCAP) return fail(c, TB_EINVAL, "cap must lie in [1, 128]");
-  if (chi_cut < 1) return fail(c, TB_EINVAL, "chi_cut must be >= 1");
+  if (chi_cut < 1 || chi_cut > cap) return fail(c, TB_EINVAL, "chi_cut must lie in [1, cap]");
   return TB_OK;
 }
 
-int launch_ensemble(tb_ctx* c, tb::Job& job, int grid, cudaStream_t st, float* kernel_ms) {
-  const size_t smem = tb::kTileBytes;
-  TB_CUDA(c, cudaFuncSetAttribute(tb::ensemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (kernel_ms) TB_CUDA(c, cudaEventRecord(c->e0, st));
-  tb::ensemble_kernel<<<grid, tb::NT, smem, st>>>(job);
-  TB_CUDA(c, cudaGetLastError());
-  if (kernel_ms) {
-    TB_CUDA(c, cudaEventRecord(c->e1, st));
-    TB_CUDA(c, cudaEventSynchronize(c->e1));
-    TB_CUDA(c, cudaEventElapsedTime(kernel_ms, c->e0, c->e1));
-  }
-  return TB_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int tb_version(void) { return 1; }
-
-int tb_create(int device, tb_ctx** out) {
-  if (!out) return TB_EINVAL;
-  *out = nullptr;
-  tb_ctx* c = new tb_ctx();
-  c->device = device;
-  if (cudaSetDevice(device) != cudaSuccess) {
-    cudaGetLastError();
-    delete c;
-    return TB_ECUDA;
-  }
-  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMalloc(&c->dscratch, 256 * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&c->dflops, 4096 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&c->dcounters, 8 * sizeof(double)) != cudaSuccess ||
-      cudaEventCreate(&c->e0) != cudaSuccess || cudaEventCreate(&c->e1) != cudaSuccess) {
-    cudaGetLastError();
-    delete c;
-    return TB_ECUDA;
-  }
-  *out = c;
-  return TB_OK;
-}
-
-void tb_destroy(tb_ctx* c) {
-  if (!c) return;
-  cudaFree(c->mps);
-  cudaFree(c->W);
-  cudaFree(c->W0);
-  cudaFree(c->X);
-  cudaFree(c->dscratch);
-  cudaFree(c->dflops);
-  cudaFree(c->dcounters);
-  if (c->e0) cudaEventDestroy(c->e0);
-  if (c->e1) cudaEventDestroy(c->e1);
-  delete c;
-}
-
-const char* tb_last_error(const tb_ctx* c) { return c ? c->err.c_str() : "null context"; }
-
-int tb_num_sms(const tb_ctx* c) { return c ? c->sms : 0; }
-
-int tb_run_stream(tb_ctx* c, double* buf, int64_t n, int64_t cap, int64_t* dims, int64_t center, const int64_t* ga,
-                  const int64_t* gb, const int64_t* pa, const int64_t* pb, const double* ang, const int64_t* anchors,
-                  int64_t n_gates, int64_t chi_cut, double floor, double* counters, int64_t* new_center) {
-  if (!c) return TB_EINVAL;
-  int rc = validate_shape(c, n, cap, chi_cut);
-  if (rc) return rc;
-  if (chi_cut > cap) return fail(c, TB_EINVAL, "chi_cut exceeds the buffer capacity");
-  if (!buf || !dims || !counters || !new_center || (n_gates > 0 && (!ga || !gb || !pa || !pb || !ang || !anchors)))
-    return fail(c, TB_EINVAL, "null argument");
-  for (int64_t s = 0; s <= n; ++s)
-    if (dims[s] < 1 || dims[s] > cap) return fail(c, TB_EINVAL, "bond dimension outside [1, cap]");
-  if (center < 0 || center >= n) return fail(c, TB_EINVAL, "center outside [0, n)");
-  // pack the lowered stream (angle table of distinct angles, <= 1024)
-  std::vector<uint32_t> words((size_t)n_gates);
-  std::vector<double> angles, table;
-  for (int64_t i = 0; i < n_gates; ++i) {
-    const int64_t a = ga[i], b = gb[i];
-    if (a < 0 || a >= n || b >= n || (b >= 0 && b <= a)) return fail(c, TB_EINVAL, "gate support outside the chain");
-    if (pa[i] < 1 || pa[i] > 3 || (b >= 0 && (pb[i] < 1 || pb[i] > 3))) return fail(c, TB_EINVAL, "bad Pauli code");
-    size_t ai = 0;
-    while (ai < angles.size() && angles[ai] != ang[i]) ++ai;
-    if (ai == angles.size()) {
-      if (angles.size() == 1024) return fail(c, TB_EINVAL, "more than 1024 distinct angles in one call");
-      angles.push_back(ang[i]);
-      table.push_back(cos(0.5 * ang[i]));
-      table.push_back(sin(0.5 * ang[i]));
-    }
-    uint32_t w = (uint32_t)a | ((b < 0 ? TB_ONE_SITE : (uint32_t)b) << 8) | ((uint32_t)pa[i] << 16) |
-                 ((uint32_t)(b < 0 ? 0 : pb[i]) << 18) | ((uint32_t)(anchors[i] > a) << 20) |
-                 ((uint32_t)(ang[i] == M_PI) << 21) | ((uint32_t)ai << 22);
-    words[(size_t)i] = w;
-  }
-  if (table.empty()) table = {1.0, 0.0};
-  rc = ensure_workspace(c, 1, (int)n, (int)cap);
-  if (rc) return rc;
-  uint32_t* dg = nullptr;
-  int64_t* doff = nullptr;
-  double* dtab = nullptr;
-  const size_t gbytes = words.size() * sizeof(uint32_t) + 4;
-  TB_CUDA(c, cudaMalloc(&dg, gbytes));
-  TB_CUDA(c, cudaMalloc(&doff, 2 * sizeof(int64_t)));
-  TB_CUDA(c, cudaMalloc(&dtab, table.size() * sizeof(double)));
-  int64_t off[2] = {0, n_gates};
-  std::vector<int> idims((size_t)n + 1);
-  for (int64_t s = 0; s <= n; ++s) idims[(size_t)s] = (int)dims[s];
-  int hs[2] = {0, 0};
-  int icenter = (int)center;
-  cudaMemcpy(dg, words.data(), words.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
-  cudaMemcpy(doff, off, sizeof(off), cudaMemcpyHostToDevice);
-  cudaMemcpy(dtab, table.data(), table.size() * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->dscratch, hs, sizeof(hs), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->dscratch + 2, &icenter, sizeof(int), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->dscratch + 3, idims.data(), idims.size() * sizeof(int), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->dcounters, counters, 4 * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemset(c->dflops, 0, sizeof(double));
-  const size_t site_bytes = (size_t)n * cap * 2 * cap * sizeof(double2);
-  cudaMemcpy(c->mps, buf, site_bytes, cudaMemcpyHostToDevice);
-  TB_CUDA(c, cudaGetLastError());
-
-  tb::Job job;
-  memset(&job, 0, sizeof(job));
-  job.n = (int)n;
-  job.cap = (int)cap;
-  job.chi_cut = (int)chi_cut;
-  job.pi_local = 0;  // drop-in: the reference's full update for pi gates
-  job.floor = floor;
-  job.n_samples = 1;
-  job.gates = dg;
-  job.gate_off = doff;
-  job.angle_cs = dtab;
-  job.next_sample = c->dscratch;
-  job.status = c->dscratch + 1;
-  job.io_center = c->dscratch + 2;
-  job.io_dims = c->dscratch + 3;
-  job.io_counters = c->dcounters;
-  job.flops = c->dflops;
-  job.ws_mps = c->mps;
-  job.ws_W = c->W;
-  job.ws_W0 = c->W0;
-  job.ws_X = c->X;
-  job.mps_stride = c->mps_stride;
-  job.mat_stride = c->mat_stride;
-  rc = launch_ensemble(c, job, 1, 0, nullptr);
-  if (rc == TB_OK) {
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) rc = fail(c, TB_ECUDA, std::string("kernel: ") + cudaGetErrorString(e));
-  }
-  if (rc == TB_OK) {
-    cudaMemcpy(buf, c->mps, site_bytes, cudaMemcpyDeviceToHost);
-    cudaMemcpy(hs, c->dscratch, sizeof(hs), cudaMemcpyDeviceToHost);
-    cudaMemcpy(&icenter, c->dscratch + 2, sizeof(int), cudaMemcpyDeviceToHost);
-    cudaMemcpy(idims.data(), c->dscratch + 3, idims.size() * sizeof(int), cudaMemcpyDeviceToHost);
-    cudaMemcpy(counters, c->dcounters, 4 * sizeof(double), cudaMemcpyDeviceToHost);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) rc = fail(c, TB_ECUDA, cudaGetErrorString(e));
-    for (int64_t s = 0; s <= n; ++s) dims[s] = idims[(size_t)s];
-    *new_center = icenter;
-    if (rc == TB_OK && (hs[1] & 1)) rc = fail(c, TB_ENOCONV, "Jacobi SVD did not converge");
-  }
-  cudaFree(dg);
-  cudaFree(doff);
-  cudaFree(dtab);
-  return rc;
-}
-
-int tb_expectation(tb_ctx* c, const double* buf, int64_t n, int64_t cap, const int64_t* dims, const int32_t* codes,
-                   double* out) {
-  if (!c) return TB_EINVAL;
-  int rc = validate_shape(c, n, cap, 1);
-  if (rc) return rc;
-  if (!buf || !dims || !codes || !out) return fail(c, TB_EINVAL, "null argument");
-  for (int64_t s = 0; s <= n; ++s)
-    if (dims[s] < 1 || dims[s] > cap) return fail(c, TB_EINVAL, "bond dimension outside [1, cap]");
-  for (int64_t s = 0; s < n; ++s)
-    if (codes[s] < 0 || codes[s] > 3) return fail(c, TB_EINVAL, "bad Pauli code");
-  rc = ensure_workspace(c, 1, (int)n, (int)cap);
-  if (rc) return rc;
-  std::vector<int> idims((size_t)n + 1);
-  for (int64_t s = 0; s <= n; ++s) idims[(size_t)s] = (int)dims[s];
-  int* dd = nullptr;
-  TB_CUDA(c, cudaMalloc(&dd, (2 * n + 1) * sizeof(int)));
-  cudaMemcpy(dd, idims.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice);
-  cudaMemcpy(dd + n + 1, codes, n * sizeof(int), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->mps, buf, (size_t)n * cap * 2 * cap * sizeof(double2), cudaMemcpyHostToDevice);
-  const size_t smem = tb::kTileBytes;
-  cudaFuncSetAttribute(tb::expectation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tb::expectation_kernel<<<1, tb::NT, smem>>>(c->mps, (int)n, (int)cap, dd, dd + n + 1, c->W, c->W0, c->dflops);
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) e = cudaMemcpy(out, c->dflops, sizeof(double), cudaMemcpyDeviceToHost);
-  cudaFree(dd);
-  if (e != cudaSuccess) return fail(c, TB_ECUDA, std::string("expectation: ") + cudaGetErrorString(e));
-  return TB_OK;
-}
-
-int tb_svd(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n, double* s, double* u, double* vh) {
-  if (!c) return TB_EINVAL;
-  if (!a || !s || batch < 1 || m < 1 || n < 1) return fail(c, TB_EINVAL, "bad arguments");
-  if (m > tb::MAXDIM || n > tb::MAXDIM) return fail(c, TB_EINVAL, "matrix larger than 256");
-  const int64_t k = m < n ? m : n;
-  const int cap = (int)((m > n ? m : n) + 1) / 2;
-  int rc = ensure_workspace(c, (int)batch, 1, cap < 1 ? 1 : cap);
-  if (rc) return rc;
-  double2 *da = nullptr, *du = nullptr, *dvh = nullptr;
-  double* ds = nullptr;
-  TB_CUDA(c, cudaMalloc(&da, batch * m * n * sizeof(double2)));
-  TB_CUDA(c, cudaMalloc(&ds, batch * k * sizeof(double)));
-  if (u) TB_CUDA(c, cudaMalloc(&du, batch * m * k * sizeof(double2)));
-  if (vh) TB_CUDA(c, cudaMalloc(&dvh, batch * k * n * sizeof(double2)));
-  cudaMemcpy(da, a, batch * m * n * sizeof(double2), cudaMemcpyHostToDevice);
-  cudaMemset(c->dscratch, 0, 2 * sizeof(int));
-  const size_t smem = tb::kTileBytes;
-  cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->mat_stride, ds, du, dvh,
-                                               c->dscratch + 1);
-  cudaError_t e = cudaDeviceSynchronize();
-  int st[2] = {0, 0};
-  if (e == cudaSuccess) {
-    cudaMemcpy(s, ds, batch * k * sizeof(double), cudaMemcpyDeviceToHost);
-    if (u) cudaMemcpy(u, du, batch * m * k * sizeof(double2), cudaMemcpyDeviceToHost);
-    if (vh) cudaMemcpy(vh, dvh, batch * k * n * sizeof(double2), cudaMemcpyDeviceToHost);
-    e = cudaMemcpy(st, c->dscratch, sizeof(st), cudaMemcpyDeviceToHost);
-  }
-  cudaFree(da);
-  cudaFree(ds);
-  cudaFree(du);
-  cudaFree(dvh);
-  if (e != cudaSuccess) return fail(c, TB_ECUDA, std::string("svd: ") + cudaGetErrorString(e));
-  if (st[1] & 1) return fail(c, TB_ENOCONV, "Jacobi SVD did not converge");
-  return TB_OK;
-}
-
-int tb_run_ensemble_device(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o, void* stream) {
-  if (!c || !d || !o) return TB_EINVAL;
+int validate_desc(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o) {
   int rc = validate_shape(c, d->n, d->cap, d->chi_cut);
   if (rc) return rc;
-  if (d->chi_cut > d->cap) return fail(c, TB_EINVAL, "chi_cut exceeds cap");
-  if (d->n_samples < 0 || d->n_ckpt < 0 || d->n_obs < 0 || d->n_obs > tb::MAXN)
+  if (d->n_samples < 0 || d->n_ckpt < 0 || d->n_obs < 0 || d->n_obs > tb::MAXN || d->n_angles < 1 ||
+      d->n_angles > 1024)
     return fail(c, TB_EINVAL, "bad ensemble sizes");
   if (!d->gates || !d->gate_offsets || !d->angle_cs || !d->init_vecs || !o->sum_v || !o->sum_v2 || !o->flops)
     return fail(c, TB_EINVAL, "null argument");
   if (d->n_ckpt > 0 && (!d->ckpt_gate_end || !d->ckpt_sign || (d->n_obs > 0 && !d->obs_sites)))
     return fail(c, TB_EINVAL, "null checkpoint argument");
-  if (d->n_samples == 0) return TB_OK;
-  const int grid = d->n_samples < c->sms ? d->n_samples : c->sms;
-  rc = ensure_workspace(c, grid, d->n, d->cap);
-  if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  TB_CUDA(c, cudaMemsetAsync(c->dscratch, 0, 2 * sizeof(int), st));
-  TB_CUDA(c, cudaMemsetAsync(c->dflops, 0, grid * sizeof(double), st));
+  return TB_OK;
+}
+
+tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o) {
   tb::Job job;
   memset(&job, 0, sizeof(job));
   job.n = d->n;
@@ -1321,103 +1687,377 @@ int tb_run_ensemble_device(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out
   job.sum_v = (unsigned long long*)o->sum_v;
   job.sum_v2 = (unsigned long long*)o->sum_v2;
   job.flops = c->dflops;
+  job.prof = c->dprof;
   job.next_sample = c->dscratch;
   job.status = c->dscratch + 1;
+  job.slot_dims = c->slot_dims;
+  job.slot_center = c->slot_center;
+  job.slot_counters = c->slot_counters;
   job.ws_mps = c->mps;
   job.ws_W = c->W;
   job.ws_W0 = c->W0;
   job.ws_X = c->X;
   job.mps_stride = c->mps_stride;
   job.mat_stride = c->mat_stride;
-  rc = launch_ensemble(c, job, grid, st, o->kernel_ms);
-  if (rc) return rc;
-  tb::sum_flops_kernel<<<1, 32, 0, st>>>(c->dflops, grid, o->flops);
+  return job;
+}
+
+// launch the persistent kernel (+ FLOP reduction into o_flops) on stream st
+int launch(tb_ctx* c, tb::Job& job, int grid, cudaStream_t st, double* o_flops, float* kernel_ms) {
+  const size_t smem = tb::kDynSmem;
+  TB_CUDA(c, cudaFuncSetAttribute(tb::ensemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TB_CUDA(c, cudaMemsetAsync(c->dscratch, 0, 2 * sizeof(int), st));
+  TB_CUDA(c, cudaMemsetAsync(c->dflops, 0, grid * sizeof(double), st));
+  TB_CUDA(c, cudaMemsetAsync(c->dprof, 0, 64 * sizeof(unsigned long long), st));
+  if (kernel_ms) TB_CUDA(c, cudaEventRecord(c->e0, st));
+  tb::ensemble_kernel<<<grid, tb::NT, smem, st>>>(job);
   TB_CUDA(c, cudaGetLastError());
+  if (kernel_ms) TB_CUDA(c, cudaEventRecord(c->e1, st));
+  if (o_flops) {
+    tb::sum_flops_kernel<<<1, 32, 0, st>>>(c->dflops, grid, o_flops);
+    TB_CUDA(c, cudaGetLastError());
+  }
+  if (kernel_ms) {
+    TB_CUDA(c, cudaEventSynchronize(c->e1));
+    TB_CUDA(c, cudaEventElapsedTime(kernel_ms, c->e0, c->e1));
+  }
   return TB_OK;
 }
 
-}  // extern "C"
+int read_status(tb_ctx* c) {
+  int st[2] = {0, 0};
+  TB_CUDA(c, cudaMemcpy(st, c->dscratch, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st[1] & 1) return fail(c, TB_ENOCONV, "Jacobi SVD did not converge");
+  return TB_OK;
+}
 
-extern "C" int tb_run_ensemble(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o) {
-  if (!c || !d || !o) return TB_EINVAL;
-  if (d->n_samples <= 0) return TB_OK;
+// device copies of a host descriptor/outputs; frees on destruction
+struct Staged {
+  std::vector<void*> allocs;
+  ~Staged() {
+    for (void* p : allocs) cudaFree(p);
+  }
+  template <class T>
+  T* up(const T* h, size_t count, bool copy = true) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, count ? count * sizeof(T) : 8) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    if (copy && h && count) cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice);
+    return (T*)p;
+  }
+};
+
+int stage_inputs(tb_ctx* c, Staged& sg, const tb_ensemble_desc* d, tb_ensemble_desc* dd) {
   const int S = d->n_samples, C = d->n_ckpt, O = d->n_obs;
   const int64_t G = d->gate_offsets[S];
-  std::vector<void*> allocs;
-  auto dalloc = [&](size_t bytes) -> void* {
-    void* p = nullptr;
-    if (cudaMalloc(&p, bytes ? bytes : 8) != cudaSuccess) return nullptr;
-    allocs.push_back(p);
-    return p;
-  };
-  auto cleanup = [&]() {
-    for (void* p : allocs) cudaFree(p);
-  };
-  tb_ensemble_desc dd = *d;
-  tb_ensemble_out od = *o;
-  uint32_t* g = (uint32_t*)dalloc(G * sizeof(uint32_t));
-  int64_t* off = (int64_t*)dalloc((S + 1) * sizeof(int64_t));
-  int32_t* ce = (int32_t*)dalloc((size_t)S * C * sizeof(int32_t));
-  int8_t* cs = (int8_t*)dalloc((size_t)S * C);
-  double* ang = (double*)dalloc(2 * d->n_angles * sizeof(double));
-  int32_t* obs = (int32_t*)dalloc(O * sizeof(int32_t));
-  double* iv = (double*)dalloc(4 * d->n * sizeof(double));
-  double* vals = o->values ? (double*)dalloc((size_t)S * C * O * sizeof(double)) : nullptr;
-  double* disc = o->discarded ? (double*)dalloc((size_t)S * C * sizeof(double)) : nullptr;
-  double* led = o->ledger ? (double*)dalloc((size_t)S * 4 * sizeof(double)) : nullptr;
-  int64_t* sv = (int64_t*)dalloc((size_t)C * O * sizeof(int64_t));
-  int64_t* sv2 = (int64_t*)dalloc((size_t)C * O * sizeof(int64_t));
-  double* fl = (double*)dalloc(sizeof(double));
-  if (!g || !off || !ce || !cs || !ang || !obs || !iv || !sv || !sv2 || !fl || (o->values && !vals) ||
-      (o->discarded && !disc) || (o->ledger && !led)) {
-    cleanup();
+  *dd = *d;
+  dd->gates = sg.up(d->gates, (size_t)G);
+  dd->gate_offsets = sg.up(d->gate_offsets, (size_t)S + 1);
+  dd->ckpt_gate_end = sg.up(d->ckpt_gate_end, (size_t)S * C);
+  dd->ckpt_sign = sg.up(d->ckpt_sign, (size_t)S * C);
+  dd->angle_cs = sg.up(d->angle_cs, 2 * (size_t)d->n_angles);
+  dd->ckpt_weight = nullptr;
+  dd->obs_sites = sg.up(d->obs_sites, (size_t)O);
+  dd->init_vecs = sg.up(d->init_vecs, 4 * (size_t)d->n);
+  if (!dd->gates || !dd->gate_offsets || !dd->ckpt_gate_end || !dd->ckpt_sign || !dd->angle_cs || !dd->obs_sites ||
+      !dd->init_vecs)
     return fail(c, TB_ENOMEM, "device allocation failed");
-  }
-  cudaMemcpy(g, d->gates, G * sizeof(uint32_t), cudaMemcpyHostToDevice);
-  cudaMemcpy(off, d->gate_offsets, (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice);
-  if (C) {
-    cudaMemcpy(ce, d->ckpt_gate_end, (size_t)S * C * sizeof(int32_t), cudaMemcpyHostToDevice);
-    cudaMemcpy(cs, d->ckpt_sign, (size_t)S * C, cudaMemcpyHostToDevice);
-  }
-  cudaMemcpy(ang, d->angle_cs, 2 * d->n_angles * sizeof(double), cudaMemcpyHostToDevice);
-  if (O) cudaMemcpy(obs, d->obs_sites, O * sizeof(int32_t), cudaMemcpyHostToDevice);
-  cudaMemcpy(iv, d->init_vecs, 4 * d->n * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(sv, o->sum_v, (size_t)C * O * sizeof(int64_t), cudaMemcpyHostToDevice);
-  cudaMemcpy(sv2, o->sum_v2, (size_t)C * O * sizeof(int64_t), cudaMemcpyHostToDevice);
-  cudaMemset(fl, 0, sizeof(double));
-  dd.gates = g;
-  dd.gate_offsets = off;
-  dd.ckpt_gate_end = ce;
-  dd.ckpt_sign = cs;
-  dd.angle_cs = ang;
-  dd.obs_sites = obs;
-  dd.init_vecs = iv;
-  od.values = vals;
-  od.discarded = disc;
-  od.ledger = led;
-  od.sum_v = sv;
-  od.sum_v2 = sv2;
-  od.flops = fl;
-  int rc = tb_run_ensemble_device(c, &dd, &od, nullptr);
-  if (rc == TB_OK) {
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) rc = fail(c, TB_ECUDA, std::string("ensemble kernel: ") + cudaGetErrorString(e));
-  }
-  if (rc == TB_OK) {
-    if (vals) cudaMemcpy(o->values, vals, (size_t)S * C * O * sizeof(double), cudaMemcpyDeviceToHost);
-    if (disc) cudaMemcpy(o->discarded, disc, (size_t)S * C * sizeof(double), cudaMemcpyDeviceToHost);
-    if (led) cudaMemcpy(o->ledger, led, (size_t)S * 4 * sizeof(double), cudaMemcpyDeviceToHost);
-    cudaMemcpy(o->sum_v, sv, (size_t)C * O * sizeof(int64_t), cudaMemcpyDeviceToHost);
-    cudaMemcpy(o->sum_v2, sv2, (size_t)C * O * sizeof(int64_t), cudaMemcpyDeviceToHost);
-    double f = 0;
-    cudaMemcpy(&f, fl, sizeof(double), cudaMemcpyDeviceToHost);
-    if (o->flops) o->flops[0] += f;
-    int st[2] = {0, 0};
-    cudaMemcpy(st, c->dscratch, sizeof(st), cudaMemcpyDeviceToHost);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) rc = fail(c, TB_ECUDA, cudaGetErrorString(e));
-    else if (st[1] & 1) rc = fail(c, TB_ENOCONV, "Jacobi SVD did not converge");
-  }
-  cleanup();
-  return rc;
+  return TB_OK;
 }
+
+int stage_outputs(tb_ctx* c, Staged& sg, const tb_ensemble_desc* d, const tb_ensemble_out* o, tb_ensemble_out* od) {
+  const int S = d->n_samples, C = d->n_ckpt, O = d->n_obs;
+  *od = *o;
+  od->values = o->values ? sg.up<double>(nullptr, (size_t)S * C * O, false) : nullptr;
+  od->discarded = o->discarded ? sg.up<double>(nullptr, (size_t)S * C, false) : nullptr;
+  od->ledger = o->ledger ? sg.up<double>(nullptr, (size_t)S * 4, false) : nullptr;
+  // sums: the caller's arrays are accumulated into, so they travel both ways
+  const size_t rows = (size_t)(o->sum_v ? 1 : 0);
+  (void)rows;
+  od->flops = sg.up<double>(nullptr, 1, false);
+  od->kernel_ms = o->kernel_ms;
+  if ((o->values && !od->values) || (o->discarded && !od->discarded) || (o->ledger && !od->ledger) || !od->flops)
+    return fail(c, TB_ENOMEM, "device allocation failed");
+  TB_CUDA(c, cudaMemset(od->flops, 0, sizeof(double)));
+  return TB_OK;
+}
+
+int fetch_outputs(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o, const tb_ensemble_out* od, size_t sum_rows) {
+  const int S = d->n_samples, C = d->n_ckpt, O = d->n_obs;
+  if (o->values) TB_CUDA(c, cudaMemcpy(o->values, od->values, (size_t)S * C * O * sizeof(double), cudaMemcpyDeviceToHost));
+  if (o->discarded)
+    TB_CUDA(c, cudaMemcpy(o->discarded, od->discarded, (size_t)S * C * sizeof(double), cudaMemcpyDeviceToHost));
+  if (o->ledger) TB_CUDA(c, cudaMemcpy(o->ledger, od->ledger, (size_t)S * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+  TB_CUDA(c, cudaMemcpy(o->sum_v, od->sum_v, sum_rows * O * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  TB_CUDA(c, cudaMemcpy(o->sum_v2, od->sum_v2, sum_rows * O * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  double f = 0;
+  TB_CUDA(c, cudaMemcpy(&f, od->flops, sizeof(double), cudaMemcpyDeviceToHost));
+  o->flops[0] += f;
+  return TB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tb_version(void) { return 1; }
+
+int tb_create(int device, tb_ctx** out) {
+  if (!out) return TB_EINVAL;
+  *out = nullptr;
+  tb_ctx* c = new tb_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return TB_ECUDA;
+  }
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMalloc(&c->dscratch, 256 * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->dflops, 4096 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->dprof, 64 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaEventCreate(&c->e0) != cudaSuccess || cudaEventCreate(&c->e1) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return TB_ECUDA;
+  }
+  cudaMemset(c->dprof, 0, 64 * sizeof(unsigned long long));
+  *out = c;
+  return TB_OK;
+}
+
+void tb_destroy(tb_ctx* c) {
+  if (!c) return;
+  free_workspace(c);
+  cudaFree(c->dscratch);
+  cudaFree(c->dflops);
+  cudaFree(c->dprof);
+  if (c->e0) cudaEventDestroy(c->e0);
+  if (c->e1) cudaEventDestroy(c->e1);
+  delete c;
+}
+
+const char* tb_last_error(const tb_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int tb_num_sms(const tb_ctx* c) { return c ? c->sms : 0; }
+
+int tb_debug_profile(tb_ctx* c, uint64_t* out64) {
+  if (!c || !out64) return TB_EINVAL;
+  cudaError_t e = cudaMemcpy(out64, c->dprof, 64 * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? TB_OK : fail(c, TB_ECUDA, cudaGetErrorString(e));
+}
+
+int tb_run_stream(tb_ctx* c, double* buf, int64_t n, int64_t cap, int64_t* dims, int64_t center, const int64_t* ga,
+                  const int64_t* gb, const int64_t* pa, const int64_t* pb, const double* ang, const int64_t* anchors,
+                  int64_t n_gates, int64_t chi_cut, double floor, double* counters, int64_t* new_center) {
+  if (!c) return TB_EINVAL;
+  int rc = validate_shape(c, n, cap, chi_cut);
+  if (rc) return rc;
+  if (!buf || !dims || !counters || !new_center || (n_gates > 0 && (!ga || !gb || !pa || !pb || !ang || !anchors)))
+    return fail(c, TB_EINVAL, "null argument");
+  for (int64_t s = 0; s <= n; ++s)
+    if (dims[s] < 1 || dims[s] > cap) return fail(c, TB_EINVAL, "bond dimension outside [1, cap]");
+  if (center < 0 || center >= n) return fail(c, TB_EINVAL, "center outside [0, n)");
+  // pack the lowered stream with a table of its distinct angles (<= 1024)
+  std::vector<uint32_t> words((size_t)n_gates);
+  std::vector<double> angles, table;
+  for (int64_t i = 0; i < n_gates; ++i) {
+    const int64_t a = ga[i], b = gb[i];
+    if (a < 0 || a >= n || b >= n || (b >= 0 && b <= a)) return fail(c, TB_EINVAL, "gate support outside the chain");
+    if (pa[i] < 1 || pa[i] > 3 || (b >= 0 && (pb[i] < 1 || pb[i] > 3))) return fail(c, TB_EINVAL, "bad Pauli code");
+    size_t ai = 0;
+    while (ai < angles.size() && angles[ai] != ang[i]) ++ai;
+    if (ai == angles.size()) {
+      if (angles.size() == 1024) return fail(c, TB_EINVAL, "more than 1024 distinct angles in one call");
+      angles.push_back(ang[i]);
+      table.push_back(cos(0.5 * ang[i]));
+      table.push_back(sin(0.5 * ang[i]));
+    }
+    words[(size_t)i] = (uint32_t)a | ((b < 0 ? TB_ONE_SITE : (uint32_t)b) << 8) | ((uint32_t)pa[i] << 16) |
+                       ((uint32_t)(b < 0 ? 0 : pb[i]) << 18) | ((uint32_t)(anchors[i] > a) << 20) |
+                       ((uint32_t)(ang[i] == M_PI) << 21) | ((uint32_t)ai << 22);
+  }
+  if (table.empty()) table = {1.0, 0.0};
+  rc = ensure_workspace(c, 1, (int)n, (int)cap);
+  if (rc) return rc;
+  Staged sg;
+  const int64_t off[2] = {0, n_gates};
+  uint32_t* dg = sg.up(words.data(), words.size());
+  int64_t* doff = sg.up(off, 2);
+  double* dtab = sg.up(table.data(), table.size());
+  if (!dg || !doff || !dtab) return fail(c, TB_ENOMEM, "device allocation failed");
+  std::vector<int> idims((size_t)tb::MAXN + 1, 1);
+  for (int64_t s = 0; s <= n; ++s) idims[(size_t)s] = (int)dims[s];
+  int icenter = (int)center;
+  const size_t site_bytes = (size_t)n * cap * 2 * cap * sizeof(double2);
+  TB_CUDA(c, cudaMemcpy(c->slot_dims, idims.data(), idims.size() * sizeof(int), cudaMemcpyHostToDevice));
+  TB_CUDA(c, cudaMemcpy(c->slot_center, &icenter, sizeof(int), cudaMemcpyHostToDevice));
+  TB_CUDA(c, cudaMemcpy(c->slot_counters, counters, 4 * sizeof(double), cudaMemcpyHostToDevice));
+  TB_CUDA(c, cudaMemcpy(c->mps, buf, site_bytes, cudaMemcpyHostToDevice));
+  tb_ensemble_desc d;
+  memset(&d, 0, sizeof(d));
+  d.n = (int)n;
+  d.cap = (int)cap;
+  d.chi_cut = (int)chi_cut;
+  d.pi_local = 0;  // drop-in: the reference's full two-site update for pi gates
+  d.svalue_floor = floor;
+  d.n_samples = 1;
+  d.gates = dg;
+  d.gate_offsets = doff;
+  d.angle_cs = dtab;
+  tb_ensemble_out o;
+  memset(&o, 0, sizeof(o));
+  tb::Job job = make_job(c, &d, &o);
+  job.slot_mode = 1;  // continue the uploaded state (no reset)
+  rc = launch(c, job, 1, 0, nullptr, nullptr);
+  if (rc) return rc;
+  TB_CUDA(c, cudaDeviceSynchronize());
+  TB_CUDA(c, cudaMemcpy(buf, c->mps, site_bytes, cudaMemcpyDeviceToHost));
+  TB_CUDA(c, cudaMemcpy(idims.data(), c->slot_dims, idims.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  TB_CUDA(c, cudaMemcpy(&icenter, c->slot_center, sizeof(int), cudaMemcpyDeviceToHost));
+  TB_CUDA(c, cudaMemcpy(counters, c->slot_counters, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int64_t s = 0; s <= n; ++s) dims[s] = idims[(size_t)s];
+  *new_center = icenter;
+  c->state_n = c->state_cap = -1;  // slot 0 now holds a caller's state, not a pipeline slot
+  return read_status(c);
+}
+
+int tb_expectation(tb_ctx* c, const double* buf, int64_t n, int64_t cap, const int64_t* dims, const int32_t* codes,
+                   double* out) {
+  if (!c) return TB_EINVAL;
+  int rc = validate_shape(c, n, cap, 1);
+  if (rc) return rc;
+  if (!buf || !dims || !codes || !out) return fail(c, TB_EINVAL, "null argument");
+  for (int64_t s = 0; s <= n; ++s)
+    if (dims[s] < 1 || dims[s] > cap) return fail(c, TB_EINVAL, "bond dimension outside [1, cap]");
+  for (int64_t s = 0; s < n; ++s)
+    if (codes[s] < 0 || codes[s] > 3) return fail(c, TB_EINVAL, "bad Pauli code");
+  rc = ensure_workspace(c, 1, (int)n, (int)cap);
+  if (rc) return rc;
+  std::vector<int> idims((size_t)n + 1);
+  for (int64_t s = 0; s <= n; ++s) idims[(size_t)s] = (int)dims[s];
+  Staged sg;
+  int* dd = sg.up<int>(nullptr, 2 * (size_t)n + 1, false);
+  double2* dbuf = sg.up((const double2*)buf, (size_t)n * cap * 2 * cap);
+  double* dout = sg.up<double>(nullptr, 1, false);
+  if (!dd || !dbuf || !dout) return fail(c, TB_ENOMEM, "device allocation failed");
+  TB_CUDA(c, cudaMemcpy(dd, idims.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  TB_CUDA(c, cudaMemcpy(dd + n + 1, codes, n * sizeof(int), cudaMemcpyHostToDevice));
+  const size_t smem = tb::kTileBytes;
+  TB_CUDA(c, cudaFuncSetAttribute(tb::expectation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  tb::expectation_kernel<<<1, tb::NT, smem>>>(dbuf, (int)n, (int)cap, dd, dd + n + 1, c->W, c->W0, dout);
+  TB_CUDA(c, cudaGetLastError());
+  TB_CUDA(c, cudaMemcpy(out, dout, sizeof(double), cudaMemcpyDeviceToHost));
+  return TB_OK;
+}
+
+int tb_svd(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n, double* s, double* u, double* vh) {
+  if (!c) return TB_EINVAL;
+  if (!a || !s || batch < 1 || m < 1 || n < 1) return fail(c, TB_EINVAL, "bad arguments");
+  if (m > tb::MAXDIM || n > tb::MAXDIM) return fail(c, TB_EINVAL, "matrix larger than 256");
+  const int64_t k = m < n ? m : n;
+  const int cap = (int)((m > n ? m : n) + 1) / 2;
+  int rc = ensure_workspace(c, (int)batch, 1, cap < 1 ? 1 : cap);
+  if (rc) return rc;
+  c->state_n = c->state_cap = -1;
+  Staged sg;
+  double2* da = sg.up((const double2*)a, (size_t)(batch * m * n));
+  double* ds = sg.up<double>(nullptr, (size_t)(batch * k), false);
+  double2* du = u ? sg.up<double2>(nullptr, (size_t)(batch * m * k), false) : nullptr;
+  double2* dvh = vh ? sg.up<double2>(nullptr, (size_t)(batch * k * n), false) : nullptr;
+  if (!da || !ds || (u && !du) || (vh && !dvh)) return fail(c, TB_ENOMEM, "device allocation failed");
+  TB_CUDA(c, cudaMemset(c->dscratch, 0, 2 * sizeof(int)));
+  TB_CUDA(c, cudaMemset(c->dprof, 0, 64 * sizeof(unsigned long long)));
+  const size_t smem = tb::kDynSmem;
+  TB_CUDA(c, cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->mat_stride, ds, du, dvh,
+                                               c->dscratch + 1, c->dprof);
+  TB_CUDA(c, cudaGetLastError());
+  TB_CUDA(c, cudaDeviceSynchronize());
+  TB_CUDA(c, cudaMemcpy(s, ds, batch * k * sizeof(double), cudaMemcpyDeviceToHost));
+  if (u) TB_CUDA(c, cudaMemcpy(u, du, batch * m * k * sizeof(double2), cudaMemcpyDeviceToHost));
+  if (vh) TB_CUDA(c, cudaMemcpy(vh, dvh, batch * k * n * sizeof(double2), cudaMemcpyDeviceToHost));
+  return read_status(c);
+}
+
+int tb_run_ensemble_device(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o, void* stream) {
+  if (!c || !d || !o) return TB_EINVAL;
+  int rc = validate_desc(c, d, o);
+  if (rc) return rc;
+  if (d->n_samples == 0) return TB_OK;
+  const int grid = d->n_samples < c->sms ? d->n_samples : c->sms;
+  rc = ensure_workspace(c, grid, d->n, d->cap);
+  if (rc) return rc;
+  c->state_n = c->state_cap = -1;  // whole-sample runs reuse the slot memory
+  tb::Job job = make_job(c, d, o);
+  job.slot_mode = 0;
+  return launch(c, job, grid, (cudaStream_t)stream, o->flops, o->kernel_ms);
+}
+
+int tb_run_ensemble(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o) {
+  if (!c || !d || !o) return TB_EINVAL;
+  int rc = validate_desc(c, d, o);
+  if (rc) return rc;
+  if (d->n_samples == 0) return TB_OK;
+  Staged sg;
+  tb_ensemble_desc dd;
+  tb_ensemble_out od;
+  if ((rc = stage_inputs(c, sg, d, &dd)) || (rc = stage_outputs(c, sg, d, o, &od))) return rc;
+  const size_t rows = (size_t)d->n_ckpt;
+  od.sum_v = sg.up(o->sum_v, rows * d->n_obs);
+  od.sum_v2 = sg.up(o->sum_v2, rows * d->n_obs);
+  if (!od.sum_v || !od.sum_v2) return fail(c, TB_ENOMEM, "device allocation failed");
+  rc = tb_run_ensemble_device(c, &dd, &od, nullptr);
+  if (rc) return rc;
+  TB_CUDA(c, cudaDeviceSynchronize());
+  if ((rc = fetch_outputs(c, d, o, &od, rows))) return rc;
+  return read_status(c);
+}
+
+int tb_step_device(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, void* stream) {
+  if (!c || !sd || !o) return TB_EINVAL;
+  const tb_ensemble_desc* d = &sd->base;
+  int rc = validate_desc(c, d, o);
+  if (rc) return rc;
+  if (d->n_samples == 0) return TB_OK;
+  if (d->n_samples > c->sms) return fail(c, TB_EINVAL, "more slots than SMs (one persistent CTA per slot)");
+  if (!sd->reset || (d->n_ckpt > 0 && !sd->sum_row)) return fail(c, TB_EINVAL, "null reset/sum_row");
+  rc = ensure_workspace(c, d->n_samples, d->n, d->cap);
+  if (rc) return rc;
+  // a slot whose state was not built for this shape must be reset by the caller;
+  // the first call after (re)allocation is accepted only if every slot resets,
+  // which the host wrapper guarantees
+  c->state_n = d->n;
+  c->state_cap = d->cap;
+  tb::Job job = make_job(c, d, o);
+  job.slot_mode = 1;
+  job.reset = sd->reset;
+  job.sum_row = sd->sum_row;
+  return launch(c, job, d->n_samples, (cudaStream_t)stream, o->flops, o->kernel_ms);
+}
+
+int tb_step(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, int64_t sum_rows) {
+  if (!c || !sd || !o) return TB_EINVAL;
+  const tb_ensemble_desc* d = &sd->base;
+  int rc = validate_desc(c, d, o);
+  if (rc) return rc;
+  if (d->n_samples == 0) return TB_OK;
+  if (sum_rows < 1) return fail(c, TB_EINVAL, "sum_rows must be >= 1");
+  Staged sg;
+  tb_step_desc sdd;
+  tb_ensemble_out od;
+  sdd = *sd;
+  if ((rc = stage_inputs(c, sg, d, &sdd.base)) || (rc = stage_outputs(c, sg, d, o, &od))) return rc;
+  sdd.reset = sg.up(sd->reset, (size_t)d->n_samples);
+  sdd.sum_row = sg.up(sd->sum_row, (size_t)d->n_samples * d->n_ckpt);
+  od.sum_v = sg.up(o->sum_v, (size_t)sum_rows * d->n_obs);
+  od.sum_v2 = sg.up(o->sum_v2, (size_t)sum_rows * d->n_obs);
+  if (!sdd.reset || !sdd.sum_row || !od.sum_v || !od.sum_v2) return fail(c, TB_ENOMEM, "device allocation failed");
+  rc = tb_step_device(c, &sdd, &od, nullptr);
+  if (rc) return rc;
+  TB_CUDA(c, cudaDeviceSynchronize());
+  if ((rc = fetch_outputs(c, d, o, &od, (size_t)sum_rows))) return rc;
+  return read_status(c);
+}
+
+}  // extern "C"

@@ -166,3 +166,157 @@ def allreduce_sums(run: EnsembleRun, group=None) -> EnsembleRun:
     return EnsembleRun(int(t[-1]), None, None, None, t[: C * O].reshape(C, O).copy(),
                        t[C * O: 2 * C * O].reshape(C, O).copy(), run.weights, run.flops, run.kernel_ms,
                        run.wall_s, dict(run.extra))
+
+
+@dataclass
+class StepPlan:
+    """Host inputs of one pipeline step (one checkpoint segment per slot)."""
+
+    words: np.ndarray      # uint32, all slots' segments concatenated
+    offsets: np.ndarray    # int64 [S+1]
+    ckpt_end: np.ndarray   # int32 [S, 1]
+    ckpt_sign: np.ndarray  # int8 [S, 1]
+    reset: np.ndarray      # uint8 [S]
+    sum_row: np.ndarray    # int32 [S, 1]
+    completes: int         # samples finished by this step
+
+
+class SlotPipeline:
+    """Continuous batching of ensemble members over persistent GPU slots.
+
+    One slot per SM keeps its MPS resident in HBM.  Every ``step`` advances each
+    slot by one checkpoint segment of its current circuit (and measures <Z_j>);
+    a slot that finished its circuit restarts from the product state with the
+    next sample id.  Checkpoint c of every sample accumulates into estimator row
+    c, so the statistics equal those of ``run_ensemble`` on the same ids.
+    """
+
+    def __init__(self, ham: Hamiltonian, cfg: PaiConfig, seed: int, labels, policy: TruncationPolicy,
+                 checkpoints, n_slots: int | None = None, observables=None, pi_local: bool = True,
+                 device: int = 0, first_sample: int = 0, sample_stride: int = 1):
+        self.ham, self.cfg, self.seed, self.device = ham, cfg, seed, device
+        self.checkpoints = np.asarray(checkpoints, dtype=np.int64)
+        if self.checkpoints[-1] != cfg.n_steps:
+            raise ValueError("the last checkpoint must be the end of the circuit")
+        self.proto = pack_ensemble(ham, cfg, seed, [], labels, policy, self.checkpoints, observables, pi_local)
+        ctx = _lib.context(device)
+        sms = _lib.load().tb_num_sms(ctx)
+        self.n_slots = min(n_slots or sms, sms)
+        self.table = TermTable.of(ham)
+        self.next_id = first_sample
+        self.stride = sample_stride
+        self.slot_pack = [None] * self.n_slots
+        self.slot_seg = [0] * self.n_slots
+        C, O = self.checkpoints.size, self.proto.obs_sites.size
+        self.sum_v = np.zeros((C, O), np.int64)
+        self.sum_v2 = np.zeros((C, O), np.int64)
+        self.row_count = np.zeros(C, np.int64)
+        self.completed = 0
+        self.flops = 0.0
+
+    def _new_sample(self):
+        sid = self.next_id
+        self.next_id += self.stride
+        circ = sample_circuit(self.ham, self.cfg, circuit_stream(self.seed, sid), sample_id=sid)
+        return pack_sampled(circ, self.table, self.checkpoints)
+
+    def plan(self) -> StepPlan:
+        """Host-side packing of the next step (advances the host schedule)."""
+        S, C = self.n_slots, self.checkpoints.size
+        segs, reset = [], np.zeros(S, np.uint8)
+        sign = np.zeros((S, 1), np.int8)
+        row = np.zeros((S, 1), np.int32)
+        completes = 0
+        for b in range(S):
+            if self.slot_pack[b] is None or self.slot_seg[b] == C:
+                self.slot_pack[b] = self._new_sample()
+                self.slot_seg[b] = 0
+                reset[b] = 1
+            p, c = self.slot_pack[b], self.slot_seg[b]
+            lo = 0 if c == 0 else int(p.ckpt_end[c - 1])
+            segs.append(p.words[lo: int(p.ckpt_end[c])])
+            sign[b, 0] = p.ckpt_sign[c]
+            row[b, 0] = c
+            self.row_count[c] += 1
+            self.slot_seg[b] = c + 1
+            completes += int(c + 1 == C)
+        offs = np.zeros(S + 1, np.int64)
+        offs[1:] = np.cumsum([s.size for s in segs])
+        ends = np.diff(offs).astype(np.int32).reshape(S, 1)
+        return StepPlan(np.concatenate(segs).astype(np.uint32), offs, ends, sign, reset, row, completes)
+
+    def _desc(self, ptrs, S):
+        p = self.proto
+        base = _lib.EnsembleDesc(p.n, p.cap, p.chi_cut, int(p.pi_local), p.floor, S, 1, p.obs_sites.size,
+                                 p.angle_cs.shape[0], ptrs["words"], ptrs["offsets"], ptrs["ckpt_end"],
+                                 ptrs["ckpt_sign"], ptrs["angle_cs"], None, ptrs["obs"], ptrs["init"])
+        return _lib.StepDesc(base, ptrs["reset"], ptrs["sum_row"])
+
+    def step_host(self, plan: StepPlan, values: np.ndarray | None = None) -> float:
+        """End-to-end step through ``tb_step`` with host buffers; returns kernel ms."""
+        S, O = self.n_slots, self.proto.obs_sites.size
+        keep = [plan.words, plan.offsets, plan.ckpt_end, plan.ckpt_sign, plan.reset, plan.sum_row,
+                self.proto.angle_cs, self.proto.obs_sites, self.proto.init_vecs]
+        keep = [np.ascontiguousarray(x) for x in keep]
+        ptrs = dict(zip(["words", "offsets", "ckpt_end", "ckpt_sign", "reset", "sum_row", "angle_cs", "obs", "init"],
+                        [x.ctypes.data for x in keep]))
+        desc = self._desc(ptrs, S)
+        vals = values if values is not None else np.zeros((S, 1, O))
+        flops = np.zeros(1)
+        kms = np.zeros(1, np.float32)
+        out = _lib.EnsembleOut(vals.ctypes.data, None, None, self.sum_v.ctypes.data, self.sum_v2.ctypes.data,
+                               flops.ctypes.data, kms.ctypes.data)
+        ctx = _lib.context(self.device)
+        _lib.check(_lib.load().tb_step(ctx, ctypes.byref(desc), ctypes.byref(out), self.sum_v.shape[0]), ctx)
+        self.flops += float(flops[0])
+        self.completed += plan.completes
+        return float(kms[0])
+
+    def upload(self, plan: StepPlan):
+        """Device copies of a step's inputs (torch tensors on this device)."""
+        import torch
+
+        dev = torch.device("cuda", self.device)
+        t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in (
+            ("words", plan.words.view(np.int32)), ("offsets", plan.offsets), ("ckpt_end", plan.ckpt_end),
+            ("ckpt_sign", plan.ckpt_sign), ("reset", plan.reset), ("sum_row", plan.sum_row))}
+        t["completes"] = plan.completes
+        return t
+
+    def device_state(self):
+        """Device-resident constant inputs and outputs for ``step_device``."""
+        import torch
+
+        dev = torch.device("cuda", self.device)
+        S, C, O = self.n_slots, self.checkpoints.size, self.proto.obs_sites.size
+        return {
+            "angle_cs": torch.from_numpy(self.proto.angle_cs).to(dev),
+            "obs": torch.from_numpy(self.proto.obs_sites).to(dev),
+            "init": torch.from_numpy(self.proto.init_vecs).to(dev),
+            "values": torch.zeros((S, 1, O), dtype=torch.float64, device=dev),
+            "sum_v": torch.from_numpy(self.sum_v).to(dev),
+            "sum_v2": torch.from_numpy(self.sum_v2).to(dev),
+            "flops": torch.zeros(1, dtype=torch.float64, device=dev),
+        }
+
+    def step_device(self, t: dict, ds: dict, stream_ptr: int) -> None:
+        """Device-resident step through ``tb_step_device`` on ``stream_ptr``."""
+        S = self.n_slots
+        ptrs = {k: t[k].data_ptr() for k in ("words", "offsets", "ckpt_end", "ckpt_sign", "reset", "sum_row")}
+        ptrs.update(angle_cs=ds["angle_cs"].data_ptr(), obs=ds["obs"].data_ptr(), init=ds["init"].data_ptr())
+        desc = self._desc(ptrs, S)
+        out = _lib.EnsembleOut(ds["values"].data_ptr(), None, None, ds["sum_v"].data_ptr(), ds["sum_v2"].data_ptr(),
+                               ds["flops"].data_ptr(), None)
+        ctx = _lib.context(self.device)
+        _lib.check(_lib.load().tb_step_device(ctx, ctypes.byref(desc), ctypes.byref(out), stream_ptr), ctx)
+        self.completed += t["completes"]
+
+    def stats(self) -> dict:
+        """Estimator over the samples that reached each checkpoint (per-row counts)."""
+        out = {}
+        for c in range(self.checkpoints.size):
+            n = int(self.row_count[c])
+            if n:
+                st = aggregate_fixed(self.sum_v[c:c + 1], self.sum_v2[c:c + 1], n, self.proto.weights[c:c + 1])
+                out[c] = {k: v[0] for k, v in st.items()}
+        return out

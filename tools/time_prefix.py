@@ -1,0 +1,33 @@
+"""Time the engine on a prefix of a config's circuits (exploration tool).
+usage: python tools/time_prefix.py N_SITES CHI HAM_SEED CIRC_SEED STEPS T N_SAMPLES MAX_STEP"""
+import math, sys, time
+import numpy as np
+sys.path.insert(0, ".")
+import paper_2604_13144_b200 as tb
+from paper_2604_13144_b200 import packing, ensemble
+
+n, chi, hs, cs, steps, T, ns, mx = (int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]),
+                                     int(sys.argv[5]), float(sys.argv[6]), int(sys.argv[7]), int(sys.argv[8]))
+ham = tb.build_spin_ring(n, 1.0, hs)
+cfg = tb.PaiConfig(math.pi / 2**7, steps, T)
+ck = np.arange(10, mx + 1, 10)
+table = packing.TermTable.of(ham)
+t0 = time.time()
+ps = [packing.pack_sampled(tb.sample_circuit(ham, cfg, tb.circuit_stream(cs, i), sample_id=i).prefix(mx), table, ck)
+      for i in range(ns)]
+w, off, ce, sg = packing.pack_batch(ps, ck.size)
+t1 = time.time()
+p = ensemble.PackedEnsemble(n, min(chi, 2 ** (n // 2)), min(chi, 2 ** (n // 2)), 1e-12, w, off, ce, sg,
+                            packing.angle_table(packing.tepai_angles(cfg.delta)),
+                            ensemble.checkpoint_weights(ham, cfg, ck), np.arange(n, dtype=np.int32),
+                            np.stack([tb.mps.SITE_VECTORS[c] for c in "01" * (n // 2)]).view(np.float64).reshape(n, 4).copy(),
+                            np.arange(ns), np.diff(off), True)
+r = ensemble.run_packed(p)
+print(f"n={n} chi={chi} samples={ns} max_step={mx} gates={w.size} pack_s={t1-t0:.2f} kernel_ms={r.kernel_ms:.1f} "
+      f"wall_s={r.wall_s:.2f} flops={r.flops:.3e} TF/s={r.flops/r.kernel_ms/1e9:.3f} "
+      f"updates={r.ledger[:,0].sum():.0f} chi3={r.ledger[:,1].sum():.3e} disc={r.ledger[:,3].mean():.2e}")
+from paper_2604_13144_b200 import _lib
+pr = _lib.debug_profile().astype(np.float64)
+tot = pr[7]
+print("phase share: jacobi %.3f qr %.3f gemm+gate %.3f post %.3f measure %.3f | calls %d avg sweeps %.2f | 128x128: calls %d avg sweeps %.2f avg Mcyc %.3f" % (
+    pr[0]/tot, pr[3]/tot, pr[4]/tot, pr[5]/tot, pr[6]/tot, pr[1], pr[2]/max(pr[1],1), pr[10], pr[11]/max(pr[10],1), pr[9]/max(pr[10],1)/1e6))

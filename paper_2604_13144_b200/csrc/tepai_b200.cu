@@ -17,6 +17,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -75,6 +76,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // ----------------------------------------------------------------------------
 struct Job {
   int n, cap, chi_cut, pi_local;
+  int precond;  // QR-preconditioned Jacobi for problems >= 32 x 32
   double floor;
   int n_samples, n_ckpt, n_obs;
   const uint32_t* gates;
@@ -113,6 +115,9 @@ struct Smem {
   int dims[MAXN + 1];
   double sig[MAXDIM];
   double nrm[4 * 32];
+  double nref[4 * 32];
+  int qperm[4 * 32];
+  int qpinv[MAXDIM];
   int perm[MAXDIM];
   double2 rco[MAXDIM];
   double red[NWARP * 4];
@@ -841,6 +846,200 @@ __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* 
 }
 
 // ----------------------------------------------------------------------------
+// Column-pivoted QR preconditioner (Businger-Golub pivoting, modified
+// Gram-Schmidt updates; only R is kept).  For the left singular vectors of W
+// (Mw x Nw) factor Y = W^H (Nw x Mw): Y Pi = Q R, so W = Pi L Q^H with
+// L = R^H (Mw x r, lower trapezoidal), and the left singular vectors of W are
+// Pi times those of L.  One-sided Jacobi on L converges in a few sweeps
+// (Drmac-Veselic preconditioning) instead of the ~15 it needs on W.
+//
+// Y (global, col-major, ld = Nw) is staged as: columns < 96 in the three
+// smem slots, columns 96..127 in registers (2 per warp).  R goes to global
+// (row-major, ld = Mw, indexed by the ORIGINAL column), the pivot order to
+// sm.qperm.  Returns the numerical rank r (residual columns below the dead
+// threshold end the factorisation).
+// ----------------------------------------------------------------------------
+template <int RPL>
+__device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, double2* smem) {
+  constexpr int LD = 32 * RPL;
+  constexpr uint32_t CB = LD * 16u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t qaddr = base + 3u * JB * CB;  // q buffer after the slots
+  const int nsm = min(Mw, 3 * JB);
+  // stage the smem columns (zero padded rows)
+  for (int e = threadIdx.x; e < nsm * LD; e += NT) {
+    const int c = e / LD, y = e - c * LD;
+    smem[e] = (y < Nw) ? Y[(size_t)c * Nw + y] : cz();
+  }
+  // register columns 96 + 2w, 97 + 2w
+  Col<RPL> g0, g1;
+  const int c0 = 3 * JB + 2 * warp, c1 = c0 + 1;
+  col_load_g(g0, Y + (size_t)c0 * Nw, c0 < Mw ? Nw : 0);
+  col_load_g(g1, Y + (size_t)c1 * Nw, c1 < Mw ? Nw : 0);
+  __syncthreads();
+  // exact column norms
+  for (int c = warp; c < nsm; c += NWARP) {
+    Col<RPL> v;
+    col_lds(v, base + (uint32_t)c * CB);
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) acc += abs2(v.v[q]);
+    acc = warp_sum(acc);
+    if (lane == 0) sm.nrm[c] = sm.nref[c] = acc;
+  }
+  {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      a0 += abs2(g0.v[q]);
+      a1 += abs2(g1.v[q]);
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    if (lane == 0) {
+      if (c0 < Mw) sm.nrm[c0] = sm.nref[c0] = a0;
+      if (c1 < Mw) sm.nrm[c1] = sm.nref[c1] = a1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int c = 0; c < Mw; ++c) t += sm.nrm[c];
+    sm.scale = 1e-28 * t;  // dead threshold on residual norm^2
+  }
+  __syncthreads();
+  const double dead = sm.scale;
+  const int rmax = min(Mw, Nw);
+  int j = 0;
+  for (; j < rmax; ++j) {
+    // pivot: largest remaining residual norm (done columns carry -1)
+    if (warp == 0) {
+      double best = -1.0;
+      int bi = -1;
+      for (int c = lane; c < Mw; c += 32) {
+        const double v = sm.nrm[c];
+        if (v > best) { best = v; bi = c; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        sm.k = (best > dead) ? bi : -1;
+        if (bi >= 0 && best > dead) {
+          sm.qperm[j] = bi;
+          sm.nrm[bi] = -1.0;
+        }
+      }
+    }
+    __syncthreads();
+    const int p = sm.k;
+    if (p < 0) break;
+    // owner normalises the pivot column into the q buffer
+    const int owner = (p < 3 * JB) ? (p % NWARP) : ((p - 3 * JB) >> 1);
+    if (warp == owner) {
+      Col<RPL> v;
+      if (p < 3 * JB) col_lds(v, base + (uint32_t)p * CB);
+      else v = (p == c0) ? g0 : g1;
+      double nn = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) nn += abs2(v.v[q]);
+      nn = warp_sum(nn);
+      const double rn = sqrt(nn), inv = 1.0 / rn;
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) v.v[q] = cscale(v.v[q], inv);
+      col_sts(qaddr, v);
+      if (lane == 0) R[(size_t)j * Mw + p] = make_double2(rn, 0.0);
+    }
+    __syncthreads();
+    Col<RPL> qv;
+    col_lds(qv, qaddr);
+    // MGS update of every remaining column: r = q^H y, y -= r q
+    auto update = [&](Col<RPL>& y, int c) {
+      double2 d = cz();
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) cfmac(d, qv.v[q], y.v[q]);
+      d.x = warp_sum(d.x);
+      d.y = warp_sum(d.y);
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        y.v[q].x -= d.x * qv.v[q].x - d.y * qv.v[q].y;
+        y.v[q].y -= d.x * qv.v[q].y + d.y * qv.v[q].x;
+      }
+      double nr = sm.nrm[c] - abs2(d);
+      if (nr < 1e-2 * sm.nref[c]) {  // cancellation: recompute exactly
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) acc += abs2(y.v[q]);
+        nr = warp_sum(acc);
+        if (lane == 0) sm.nref[c] = nr;
+      }
+      if (lane == 0) {
+        sm.nrm[c] = nr;
+        R[(size_t)j * Mw + c] = d;
+      }
+    };
+    for (int c = warp; c < nsm; c += NWARP) {
+      if (sm.nrm[c] < 0.0) continue;
+      Col<RPL> y;
+      col_lds(y, base + (uint32_t)c * CB);
+      update(y, c);
+      col_sts(base + (uint32_t)c * CB, y);
+    }
+    if (c0 < Mw && sm.nrm[c0] >= 0.0) update(g0, c0);
+    if (c1 < Mw && sm.nrm[c1] >= 0.0) update(g1, c1);
+    __syncthreads();
+  }
+  // complete the permutation with the numerically dead columns
+  if (threadIdx.x == 0) {
+    int k = j;
+    for (int c = 0; c < Mw; ++c)
+      if (sm.nrm[c] >= 0.0) sm.qperm[k++] = c;
+    for (int k2 = 0; k2 < Mw; ++k2) sm.qpinv[sm.qperm[k2]] = k2;
+  }
+  __syncthreads();
+  return j;
+}
+
+// L = R^H in pivoted row order: L[k][i] = conj(R[i][perm[k]]) for k >= i
+// (Mw x r, column-major into W)
+__device__ void build_l(const double2* R, int Mw, int r, double2* W, const Smem& sm) {
+  for (int e = threadIdx.x; e < Mw * r; e += NT) {
+    const int i = e / Mw, k = e - i * Mw;
+    W[e] = (k >= i) ? cconj(R[(size_t)i * Mw + sm.qperm[k]]) : cz();
+  }
+  __syncthreads();
+}
+
+template <int RPL>
+__device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
+  const int r = qrcp_mgs<RPL>(W, Nw, Mw, X, sm, smem);
+  const int K = min(Mw, Nw);
+  int neff = 0;
+  if (r > 0) {
+    build_l(X, Mw, r, W, sm);
+    neff = jacobi(W, Mw, r, sm, smem, status);
+  }
+  // the numerically dead directions are exact zero columns
+  if (neff < K) {
+    for (int e = threadIdx.x; e < (K - neff) * Mw; e += NT) W[(size_t)neff * Mw + e] = cz();
+    __syncthreads();
+  }
+  return max(neff, K);
+}
+
+// Y = W^H is in W (ld = Nw); returns Neff, W = rotated columns of L (ld = Mw),
+// rows in pivoted order (sm.qpinv maps an original row to its position)
+__device__ int precond_jacobi(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
+  if (Nw <= 32) return precond_jacobi_t<1>(W, X, Mw, Nw, sm, smem, status);
+  if (Nw <= 64) return precond_jacobi_t<2>(W, X, Mw, Nw, sm, smem, status);
+  return precond_jacobi_t<4>(W, X, Mw, Nw, sm, smem, status);
+}
+
+// ----------------------------------------------------------------------------
 // Per-CTA sample context
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ long long prof_clock() { return clock64(); }
@@ -876,7 +1075,13 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   double2* W0 = cx.W0;
   const long long t0 = prof_clock();
 
-  // theta = A (2cl x cm) . B (cm x 2cr), written into W in the Jacobi orientation
+  // QR-preconditioned path for sizeable problems: W holds Y = W_jac^H, i.e.
+  // theta is written in the opposite orientation (see precond_jacobi)
+  const bool pre = jb.precond && Mw >= 32 && Nw >= 32 && Mw <= 128 && Nw <= 128;
+  const bool orient = pre ? !merge_right : merge_right;  // true: col-major theta
+  const int ldw = orient ? M : N;
+
+  // theta = A (2cl x cm) . B (cm x 2cr), written into W
   cta_gemm<true, false>(
       M, N, cm, [&](int m, int k) { return A[(size_t)m * cap + k]; },
       [&](int k, int n) {
@@ -884,8 +1089,8 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
         return B[(size_t)(k * 2 + j) * cap + r];
       },
       [&](int m, int n, double2 v) {
-        if (merge_right) W[(size_t)n * Mw + m] = v;
-        else W[(size_t)m * Mw + n] = cconj(v);
+        if (orient) W[(size_t)n * ldw + m] = v;
+        else W[(size_t)m * ldw + n] = cconj(v);
       },
       cx.tile);
 
@@ -895,14 +1100,16 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
     const int l = e / cr, r = e - (e / cr) * cr;
     double2 t[2][2];
     size_t idx[2][2];
+    size_t idw[2][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int row = l * 2 + i, col = j * cr + r;
         idx[i][j] = merge_right ? (size_t)col * Mw + row : (size_t)row * Mw + col;
-        const double2 v = W[idx[i][j]];
-        t[i][j] = merge_right ? v : cconj(v);
+        idw[i][j] = orient ? (size_t)col * ldw + row : (size_t)row * ldw + col;
+        const double2 v = W[idw[i][j]];
+        t[i][j] = orient ? v : cconj(v);
       }
     double2 o[2][2];
     if (kind == 1) {
@@ -933,16 +1140,19 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const double2 v = merge_right ? o[i][j] : cconj(o[i][j]);
-        W[idx[i][j]] = v;
-        W0[idx[i][j]] = v;
+        W[idw[i][j]] = orient ? o[i][j] : cconj(o[i][j]);
+        W0[idx[i][j]] = merge_right ? o[i][j] : cconj(o[i][j]);
       }
   }
   __syncthreads();
 
   const long long t1 = prof_clock();
   if (threadIdx.x == 0) sm.sweeps = 0;
-  const int Neff = jacobi(W, Mw, Nw, sm, cx.tile, jb.status);
+  const int Neff = pre ? precond_jacobi(W, cx.X, Mw, Nw, sm, cx.tile, jb.status) : jacobi(W, Mw, Nw, sm, cx.tile, jb.status);
+  if (!pre) {
+    for (int y = threadIdx.x; y < Mw; y += NT) sm.qpinv[y] = y;
+    __syncthreads();
+  }
   const long long t2 = prof_clock();
   prof_add(jb, 4, t1 - t0);
   prof_add(jb, 0, t2 - t1);
@@ -988,7 +1198,7 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   for (int e = threadIdx.x; e < k * Mw; e += NT) {
     const int c = e / Mw, y = e - c * Mw;
     const int pc = sm.perm[c];
-    const double2 q = cscale(W[(size_t)pc * Mw + y], 1.0 / sm.sig[pc]);
+    const double2 q = cscale(W[(size_t)pc * Mw + sm.qpinv[y]], 1.0 / sm.sig[pc]);
     if (merge_right) {
       A[(size_t)y * cap + c] = q;  // site s [(l,i)][c]
     } else {
@@ -1001,7 +1211,7 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
       k, Nw, Mw,
       [&](int c, int y) {
         const int pc = sm.perm[c];
-        return cscale(cconj(W[(size_t)pc * Mw + y]), 1.0 / sm.sig[pc]);
+        return cscale(cconj(W[(size_t)pc * Mw + sm.qpinv[y]]), 1.0 / sm.sig[pc]);
       },
       [&](int y, int x) { return W0[(size_t)x * Mw + y]; },
       [&](int c, int x, double2 v) {
@@ -1500,8 +1710,8 @@ __global__ void __launch_bounds__(NT, 1) expectation_kernel(const double2* buf, 
 // batched thin SVD (unit-test surface of the Jacobi path)
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int n, double2* Wg, double2* W0g,
-                                                    size_t mat_stride, double* s, double2* u, double2* vh,
-                                                    int* status, unsigned long long* prof) {
+                                                    double2* Xg, size_t mat_stride, double* s, double2* u,
+                                                    double2* vh, int* status, unsigned long long* prof, int precond) {
   extern __shared__ double2 dyn_smem[];
   __shared__ Smem sm;
   if (threadIdx.x == 0) sm.prof = prof;
@@ -1509,15 +1719,21 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
   const int K = min(m, n);
   double2* W = Wg + mat_stride * b;
   double2* W0 = W0g + mat_stride * b;
+  double2* X = Xg + mat_stride * b;
   const double2* A = a + (size_t)b * m * n;
-  // orthogonalise columns of A (m x n): W[c][y] = A[y][c]
+  const bool pre = precond && m >= 32 && n >= 32 && m <= 128 && n <= 128;
+  // left singular vectors of A (m x n): columns of W = A, or Y = A^H when preconditioned
   for (int e = threadIdx.x; e < m * n; e += NT) {
     const int y = e / n, c = e - y * n;
-    W[(size_t)c * m + y] = A[e];
+    if (pre) W[(size_t)y * n + c] = cconj(A[e]);
+    else W[(size_t)c * m + y] = A[e];
     W0[(size_t)c * m + y] = A[e];
   }
   __syncthreads();
-  const int Neff = jacobi(W, m, n, sm, dyn_smem, status);
+  const int Neff = pre ? precond_jacobi(W, X, m, n, sm, dyn_smem, status) : jacobi(W, m, n, sm, dyn_smem, status);
+  if (!pre)
+    for (int y = threadIdx.x; y < m; y += NT) sm.qpinv[y] = y;
+  __syncthreads();
   if (threadIdx.x == 0 && prof) {
     atomicAdd(&prof[1], 1ull);
     atomicAdd(&prof[2], (unsigned long long)sm.sweeps);
@@ -1529,7 +1745,7 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
       const int y = e / K, c = e - y * K;
       const int pc = sm.perm[c];
       const double sg = sm.sig[pc];
-      u[(size_t)b * m * K + e] = sg > 0 ? cscale(W[(size_t)pc * m + y], 1.0 / sg) : cz();
+      u[(size_t)b * m * K + e] = sg > 0 ? cscale(W[(size_t)pc * m + sm.qpinv[y]], 1.0 / sg) : cz();
     }
   if (vh)
     cta_gemm<true, true>(
@@ -1537,14 +1753,14 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
         [&](int c, int y) {
           const int pc = sm.perm[c];
           const double sg = sm.sig[pc];
-          return sg > 0 ? cscale(cconj(W[(size_t)pc * m + y]), 1.0 / (sg * sg)) : cz();
+          return sg > 0 ? cscale(cconj(W[(size_t)pc * m + sm.qpinv[y]]), 1.0 / (sg * sg)) : cz();
         },
         [&](int y, int x) { return W0[(size_t)x * m + y]; },
         [&](int c, int x, double2 v) { vh[(size_t)b * K * n + (size_t)c * n + x] = v; }, dyn_smem);
 }
 
 constexpr size_t kTileBytes = 2 * TK * TLD * sizeof(double2);
-constexpr size_t kDynSmem = 3 * JB * 128 * sizeof(double2);  // >= kTileBytes (aliased)
+constexpr size_t kDynSmem = (3 * JB + 1) * 128 * sizeof(double2);  // Jacobi/QRCP slots + q buffer; tiles alias
 static_assert(kDynSmem >= kTileBytes, "tile buffer aliases the Jacobi slots");
 
 __global__ void sum_flops_kernel(const double* f, int n, double* out) {
@@ -1670,6 +1886,10 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
   job.cap = d->cap;
   job.chi_cut = d->chi_cut;
   job.pi_local = d->pi_local;
+  {
+    const char* pe = getenv("TB_PRECOND");
+    job.precond = pe ? atoi(pe) : 1;
+  }
   job.floor = d->svalue_floor;
   job.n_samples = d->n_samples;
   job.n_ckpt = d->n_ckpt;
@@ -1970,8 +2190,10 @@ int tb_svd(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n, doub
   TB_CUDA(c, cudaMemset(c->dprof, 0, 64 * sizeof(unsigned long long)));
   const size_t smem = tb::kDynSmem;
   TB_CUDA(c, cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->mat_stride, ds, du, dvh,
-                                               c->dscratch + 1, c->dprof);
+  const char* pe = getenv("TB_PRECOND");
+  const int precond = pe ? atoi(pe) : 1;
+  tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->X, c->mat_stride, ds, du, dvh,
+                                               c->dscratch + 1, c->dprof, precond);
   TB_CUDA(c, cudaGetLastError());
   TB_CUDA(c, cudaDeviceSynchronize());
   TB_CUDA(c, cudaMemcpy(s, ds, batch * k * sizeof(double), cudaMemcpyDeviceToHost));

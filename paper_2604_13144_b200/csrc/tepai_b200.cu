@@ -348,6 +348,8 @@ __device__ void sort_sigma(const double2* W, int Mw, int Nw, Smem& sm) {
 // Every warp step processes two independent pairs so one transposed warp
 // reduction and one half-warp parameter evaluation serve both.
 // ----------------------------------------------------------------------------
+__device__ __forceinline__ long long prof_clock() { return clock64(); }
+
 constexpr int JB = 32;  // columns per block
 
 __device__ __forceinline__ double2 lds2(uint32_t a) {
@@ -1016,7 +1018,9 @@ __device__ void build_l(const double2* R, int Mw, int r, double2* W, const Smem&
 
 template <int RPL>
 __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
+  const long long t0 = prof_clock();
   const int r = qrcp_mgs<RPL>(W, Nw, Mw, X, sm, smem);
+  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[12], (unsigned long long)(prof_clock() - t0));
   const int K = min(Mw, Nw);
   int neff = 0;
   if (r > 0) {
@@ -1042,7 +1046,6 @@ __device__ int precond_jacobi(double2* W, double2* X, int Mw, int Nw, Smem& sm, 
 // ----------------------------------------------------------------------------
 // Per-CTA sample context
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ long long prof_clock() { return clock64(); }
 __device__ __forceinline__ void prof_add(const Job& jb, int slot, long long v) {
   if (threadIdx.x == 0 && jb.prof) atomicAdd(&jb.prof[slot], (unsigned long long)v);
 }

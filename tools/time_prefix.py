@@ -29,5 +29,5 @@ print(f"n={n} chi={chi} samples={ns} max_step={mx} gates={w.size} pack_s={t1-t0:
 from paper_2604_13144_b200 import _lib
 pr = _lib.debug_profile().astype(np.float64)
 tot = pr[7]
-print("phase share: jacobi %.3f qr %.3f gemm+gate %.3f post %.3f measure %.3f | calls %d avg sweeps %.2f | 128x128: calls %d avg sweeps %.2f avg Mcyc %.3f" % (
-    pr[0]/tot, pr[3]/tot, pr[4]/tot, pr[5]/tot, pr[6]/tot, pr[1], pr[2]/max(pr[1],1), pr[10], pr[11]/max(pr[10],1), pr[9]/max(pr[10],1)/1e6))
+print("phase share: jacobi %.3f (qrcp %.3f) qr %.3f gemm+gate %.3f post %.3f measure %.3f | calls %d avg sweeps %.2f | 128x128: calls %d avg sweeps %.2f avg Mcyc %.3f" % (
+    pr[0]/tot, pr[12]/tot, pr[3]/tot, pr[4]/tot, pr[5]/tot, pr[6]/tot, pr[1], pr[2]/max(pr[1],1), pr[10], pr[11]/max(pr[10],1), pr[9]/max(pr[10],1)/1e6))

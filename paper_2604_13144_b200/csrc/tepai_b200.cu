@@ -115,6 +115,11 @@ struct Smem {
   int dims[MAXN + 1];
   double sig[MAXDIM];
   double nrm[4 * 32];
+  double pbuf[NWARP][2][6];  // per-warp Jacobi parameter exchange
+  double wbest[NWARP];       // per-warp pivot candidates (QRCP)
+  int qcnt[16];              // cross-phase Q-group visit counters
+  unsigned char chg[4 * 32]; // bit0: rotated in the previous sweep, bit1: in this sweep
+  int wbidx[NWARP];
   double nref[4 * 32];
   int qperm[4 * 32];
   int qpinv[MAXDIM];
@@ -125,6 +130,7 @@ struct Smem {
   double counters[4];
   double flops;
   double scale, invsig_tmp;
+  double offmax;
   int k;
   int flag;
   int sweeps;
@@ -221,9 +227,17 @@ __device__ void cta_gemm(int M, int N, int K, LA la, LB lb, SC sc, double2* tile
 // after the first sweep without a rotation.  Returns the number of sweeps.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ void rr_pair(int r, int p, int Np, int& i, int& j) {
+  // circle method, r in [0, Np-1), p in [0, Np/2): no integer division
   const int m = Np - 1;
-  if (p == 0) { i = m; j = r; }
-  else { i = (r + p) % m; j = (r - p + m) % m; }
+  if (p == 0) {
+    i = m;
+    j = r;
+  } else {
+    i = r + p;
+    if (i >= m) i -= m;
+    j = r - p;
+    if (j < 0) j += m;
+  }
 }
 
 __device__ int hestenes(double2* W, int Mw, int Nw, Smem& sm) {
@@ -402,6 +416,9 @@ __device__ __forceinline__ void col_store_g(double2* p, const Col<RPL>& c, int M
 struct Rot {
   double c, s, er, ei, tg;
 };
+__device__ __forceinline__ void atomic_max_pos(double* a, double v) {  // v >= 0
+  atomicMax((unsigned long long*)a, (unsigned long long)__double_as_longlong(v));
+}
 
 // Jacobi parameters for one pair (alpha = |a|^2, beta = |b|^2, g = a^H b):
 // t = 2|g| sgn(d) / (|d| + sqrt(d^2 + 4|g|^2)), d = beta - alpha (the smaller
@@ -410,28 +427,44 @@ struct Rot {
 // (|g|^2 <= tol2 alpha beta) or when the rotation would move either column by
 // less than the absolute rounding floor of the matrix (|g|^2 <= abs2 *
 // max(alpha, beta)) — the same absolute accuracy LAPACK's SVD delivers.
+// Branch-free FP64 reciprocal square root / reciprocal for well-scaled
+// positive arguments: MUFU seed + Newton steps (2 steps: ~1 ulp).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_nr1(double x) {  // ~2^-44 relative
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  return y;
+}
+
 __device__ __forceinline__ Rot rot_params(double gr, double gi, double al, double be, bool valid, double tol2,
                                           double abs2) {
   Rot p;
   const double g2 = fma(gr, gr, gi * gi);
   const bool rot = valid && (g2 > tol2 * al * be) && (g2 > abs2 * fmax(al, be));
-  p.c = 1.0;
-  p.s = 0.0;
-  p.er = 1.0;
-  p.ei = 0.0;
-  p.tg = 0.0;
-  if (rot) {
-    const double ig = rsqrt(g2);
-    const double g = g2 * ig;
-    const double d = be - al;
-    const double den = fabs(d) + sqrt(fma(d, d, 4.0 * g2));
-    const double t = copysign(2.0 * g, d) / den;
-    p.c = rsqrt(fma(t, t, 1.0));
-    p.s = t * p.c;
-    p.er = gr * ig;
-    p.ei = -gi * ig;
-    p.tg = t * g;
-  }
+  // t only fixes the rotation angle (an approximate t still gives an exactly
+  // unitary rotation, c = 1/sqrt(1+t^2), s = t c); c and e = conj(g)/|g| are
+  // evaluated to full precision.
+  const double gs = rot ? g2 : 1.0;
+  const double ig = rsqrt_nr(gs);
+  const double g = gs * ig;
+  const double d = be - al;
+  const double h2 = fma(d, d, 4.0 * gs);
+  const double h = h2 * rsqrt_nr(h2);
+  const double t = copysign(2.0 * g, d) * rcp_nr1(fabs(d) + h);
+  const double c = rsqrt_nr(fma(t, t, 1.0));
+  p.c = rot ? c : 1.0;
+  p.s = rot ? t * c : 0.0;
+  p.er = rot ? gr * ig : 1.0;
+  p.ei = rot ? -gi * ig : 0.0;
+  p.tg = rot ? t * g : 0.0;
   return p;
 }
 
@@ -464,19 +497,27 @@ __device__ __forceinline__ void apply_rot(Col<RPL>& a, Col<RPL>& b, const Rot& p
 
 struct Thr {
   double tol2, abs2;
+  mutable double offmax;  // max |g|^2/(alpha beta) over rotated pairs (half-warp leaders)
 };
 
 // two independent pairs (a0,b0), (a1,b1); returns true if any rotation applied
 template <int RPL>
 __device__ __forceinline__ bool rot2(Col<RPL>& a0, Col<RPL>& b0, double& na0, double& nb0, bool v0, Col<RPL>& a1,
-                                     Col<RPL>& b1, double& na1, double& nb1, bool v1, const Thr& th) {
+                                     Col<RPL>& b1, double& na1, double& nb1, bool v1, const Thr& th, double* pb,
+                                     bool* out0 = nullptr, bool* out1 = nullptr) {
   const int lane = threadIdx.x & 31;
-  double2 g0 = cz(), g1 = cz();
+  double2 g0 = cz(), g1 = cz(), h0 = cz(), h1 = cz();
 #pragma unroll
-  for (int q = 0; q < RPL; ++q) {
+  for (int q = 0; q < RPL; q += 2) {
     cfmac(g0, a0.v[q], b0.v[q]);
     cfmac(g1, a1.v[q], b1.v[q]);
+    if (q + 1 < RPL) {
+      cfmac(h0, a0.v[q + 1], b0.v[q + 1]);
+      cfmac(h1, a1.v[q + 1], b1.v[q + 1]);
+    }
   }
+  g0 = cadd(g0, h0);
+  g1 = cadd(g1, h1);
   // transposed reduction of (g0.x, g0.y, g1.x, g1.y): lanes 0-15 end with g0,
   // lanes 16-31 with g1
   const bool up = lane & 16;
@@ -493,8 +534,26 @@ __device__ __forceinline__ bool rot2(Col<RPL>& a0, Col<RPL>& b0, double& na0, do
   z += __shfl_xor_sync(0xffffffffu, z, 1);
   const double o = __shfl_xor_sync(0xffffffffu, z, 8);
   const double gr = h8 ? o : z, gi = h8 ? z : o;
-  const Rot mine = rot_params(gr, gi, up ? na1 : na0, up ? nb1 : nb0, up ? v1 : v0, th.tol2, th.abs2);
-  const Rot p0 = shfl_rot(mine, 0), p1 = shfl_rot(mine, 16);
+  const double myal = up ? na1 : na0, mybe = up ? nb1 : nb0;
+  const Rot mine = rot_params(gr, gi, myal, mybe, up ? v1 : v0, th.tol2, th.abs2);
+  if (mine.s != 0.0 && (lane & 15) == 0) {
+    const double rel2 = fma(gr, gr, gi * gi) / (myal * mybe);
+    if (rel2 > th.offmax) th.offmax = rel2;
+  }
+  // half-warp leaders publish their pair's parameters; every lane reads both
+  double* my = pb + (up ? 6 : 0);
+  if ((lane & 15) == 0) {
+    my[0] = mine.c;
+    my[1] = mine.s;
+    my[2] = mine.er;
+    my[3] = mine.ei;
+    my[4] = mine.tg;
+  }
+  __syncwarp();
+  Rot p0, p1;
+  p0.c = pb[0]; p0.s = pb[1]; p0.er = pb[2]; p0.ei = pb[3]; p0.tg = pb[4];
+  p1.c = pb[6]; p1.s = pb[7]; p1.er = pb[8]; p1.ei = pb[9]; p1.tg = pb[10];
+  __syncwarp();
   const bool r0 = p0.s != 0.0, r1 = p1.s != 0.0;
   if (r0) apply_rot(a0, b0, p0);
   if (r1) apply_rot(a1, b1, p1);
@@ -521,6 +580,8 @@ __device__ __forceinline__ bool rot2(Col<RPL>& a0, Col<RPL>& b0, double& na0, do
     if (f2) na1 = warp_sum(e2);
     if (f3) nb1 = warp_sum(e3);
   }
+  if (out0) *out0 = r0;
+  if (out1) *out1 = r1;
   return r0 || r1;
 }
 
@@ -554,7 +615,7 @@ struct JacobiSmem {
         if (r < nbp - 1 && warp < nbp / 2) {
           int i, j;
           rr_pair(r, warp, nbp, i, j);
-          if (i < nb && j < nb) {
+          if (i < nb && j < nb && ((sm.chg[s * JB + i] | sm.chg[s * JB + j]) & 1)) {
             if (cnt == 0) { ps0 = s; is0 = i; js0 = j; }
             else if (cnt == 1) { ps1 = s; is1 = i; js1 = j; }
             else { ps2 = s; is2 = i; js2 = j; }
@@ -579,8 +640,7 @@ struct JacobiSmem {
 #pragma unroll
           for (int q = 0; q < RPL; ++q) a1.v[q] = b1.v[q] = cz();
         }
-        const bool rr = rot2<RPL>(a0, b0, na0, nb0, true, a1, b1, na1, nb1, two, th);
-        if (rr && (threadIdx.x & 31) == 0) atomicAdd(&sm.rotcount, 1);
+        const bool rr = rot2<RPL>(a0, b0, na0, nb0, true, a1, b1, na1, nb1, two, th, &sm.pbuf[warp][0][0]);
         if (rr) {
           any = true;
           col_sts(scol(pa, ia), a0);
@@ -592,9 +652,13 @@ struct JacobiSmem {
           if ((threadIdx.x & 31) == 0) {
             sm.nrm[pa * JB + ia] = na0;
             sm.nrm[pa * JB + ja] = nb0;
+            sm.chg[pa * JB + ia] |= 2;
+            sm.chg[pa * JB + ja] |= 2;
             if (two) {
               sm.nrm[ps1 * JB + is1] = na1;
               sm.nrm[ps1 * JB + js1] = nb1;
+              sm.chg[ps1 * JB + is1] |= 2;
+              sm.chg[ps1 * JB + js1] |= 2;
             }
           }
         }
@@ -605,37 +669,64 @@ struct JacobiSmem {
   }
 
   // P (registers: columns 2w, 2w+1) against smem slot sq
-  __device__ void cross(Col<RPL>& p0, Col<RPL>& p1, double& np0, double& np1, int nP, int sq, Smem& sm) {
+  __device__ void cross(Col<RPL>& p0, Col<RPL>& p1, double& np0, double& np1, int nP, int sp, int sq, Smem& sm) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nQ = ncol[sq];
     const bool vp0 = 2 * warp < nP, vp1 = 2 * warp + 1 < nP;
+    unsigned char* cp = &sm.chg[sp * JB + 2 * warp];
     bool any = false;
+    const long long tc0 = prof_clock();
+    // Q group g visits warps g, g-1, g-2, ... (round r: warp (g - r) mod 16);
+    // sm.qcnt[g] counts completed visits, so a warp waits only for the warp
+    // that held its next group in the previous round (no CTA-wide barrier)
+    if (threadIdx.x < 16) sm.qcnt[threadIdx.x] = 0;
+    __syncthreads();
     for (int r = 0; r < 16; ++r) {
       const int g = (warp + r) & 15;
       const bool vq0 = 2 * g < nQ, vq1 = 2 * g + 1 < nQ;
+      if (r > 0) {
+        if (lane == 0)
+          while (*(volatile int*)&sm.qcnt[g] < r) __nanosleep(20);
+        __syncwarp();
+        __threadfence_block();
+      }
       if ((vp0 || vp1) && (vq0 || vq1)) {
         Col<RPL> q0, q1;
         const uint32_t a0 = scol(sq, 2 * g), a1 = scol(sq, 2 * g + 1);
         col_lds(q0, a0);
         col_lds(q1, a1);
         double nq0 = sm.nrm[sq * JB + 2 * g], nq1 = sm.nrm[sq * JB + 2 * g + 1];
-        bool rr = rot2<RPL>(p0, q0, np0, nq0, vp0 && vq0, p1, q1, np1, nq1, vp1 && vq1, th);
-        const bool rr2 = rot2<RPL>(p0, q1, np0, nq1, vp0 && vq1, p1, q0, np1, nq0, vp1 && vq0, th);
-        if (lane == 0 && (rr || rr2)) atomicAdd(&sm.rotcount, (int)rr + (int)rr2);
-        rr |= rr2;
-        if (rr) {
+        double* pb = &sm.pbuf[warp][0][0];
+        unsigned char* cq = &sm.chg[sq * JB + 2 * g];
+        // a pair whose two columns were both untouched during the previous
+        // sweep was found orthogonal then and still is: skip it
+        const int fp0 = cp[0] & 1, fp1 = cp[1] & 1, fq0 = cq[0] & 1, fq1 = cq[1] & 1;
+        const bool s00 = vp0 && vq0 && (fp0 | fq0), s11 = vp1 && vq1 && (fp1 | fq1);
+        const bool s01 = vp0 && vq1 && (fp0 | fq1), s10 = vp1 && vq0 && (fp1 | fq0);
+        bool r00 = false, r11 = false, r01 = false, r10 = false;
+        if (s00 || s11) rot2<RPL>(p0, q0, np0, nq0, s00, p1, q1, np1, nq1, s11, th, pb, &r00, &r11);
+        if (s01 || s10) rot2<RPL>(p0, q1, np0, nq1, s01, p1, q0, np1, nq0, s10, th, pb, &r01, &r10);
+        if (r00 || r11 || r01 || r10) {
           any = true;
           col_sts(a0, q0);
           col_sts(a1, q1);
           if (lane == 0) {
             sm.nrm[sq * JB + 2 * g] = nq0;
             sm.nrm[sq * JB + 2 * g + 1] = nq1;
+            if (r00 || r01) cp[0] |= 2;
+            if (r11 || r10) cp[1] |= 2;
+            if (r00 || r10) cq[0] |= 2;
+            if (r11 || r01) cq[1] |= 2;
           }
         }
       }
-      __syncthreads();
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) *(volatile int*)&sm.qcnt[g] = r + 1;
     }
+    __syncthreads();
     if (any && lane == 0) sm.flag = 1;
+    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[14], (unsigned long long)(prof_clock() - tc0));
   }
 
   __device__ void load_p_smem(Col<RPL>& p0, Col<RPL>& p1, double& n0, double& n1, int s, Smem& sm) {
@@ -672,7 +763,7 @@ struct JacobiSmem {
   }
 
   // exact norms of every column; zero the numerically dead ones; thresholds
-  __device__ void refresh_norms(Smem& sm, double tol) {
+  __device__ void refresh_norms(Smem& sm, double tol, bool first) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int c = warp; c < JB * nblk; c += NWARP) {
       const int s = c / JB, k = c - s * JB;
@@ -690,6 +781,7 @@ struct JacobiSmem {
       if (lane == 0) sm.nrm[c] = acc;
     }
     __syncthreads();
+    for (int c = threadIdx.x; c < JB * nblk; c += NT) sm.chg[c] = first ? 1 : ((sm.chg[c] >> 1) & 1);
     if (threadIdx.x == 0) {
       double t = 0.0, mx = 0.0;
       for (int c = 0; c < JB * nblk; ++c) {
@@ -699,6 +791,7 @@ struct JacobiSmem {
       sm.scale = t;
       sm.invsig_tmp = mx;
       sm.flag = 0;
+      sm.offmax = 0.0;
     }
     __syncthreads();
     th.tol2 = tol * tol;
@@ -724,20 +817,45 @@ struct JacobiSmem {
   }
 
   __device__ void sweep(Smem& sm) {
+    th.offmax = 0.0;
+    sweep_body(sm);
+    if ((threadIdx.x & 15) == 0 && th.offmax > 0.0) atomic_max_pos(&sm.offmax, th.offmax);
+  }
+
+  __device__ void sweep_body(Smem& sm) {
     const int all3[3] = {0, 1, 2};
     const int nsm = min(nblk, 3);
+    const long long tw0 = prof_clock();
     within(all3, nsm, sm);
+    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[13], (unsigned long long)(prof_clock() - tw0));
     if (nblk == 4) {
       {
         Col<RPL> p0, p1;
         double n0, n1;
         load_p_g(p0, p1, n0, n1, sm);
-        for (int s = 0; s < 3; ++s) cross(p0, p1, n0, n1, ncol[3], s, sm);
+        for (int s = 0; s < 3; ++s) cross(p0, p1, n0, n1, ncol[3], 3, s, sm);
         // swap contents: A -> G storage, P (old G) -> A
         Col<RPL> t0, t1;
         double m0, m1;
         load_p_smem(t0, t1, m0, m1, 0, sm);
         __syncthreads();
+        {
+          const int warp = threadIdx.x >> 5;
+          unsigned char f0 = 0, f1 = 0, h0 = 0, h1 = 0;
+          if ((threadIdx.x & 31) == 0) {
+            f0 = sm.chg[3 * JB + 2 * warp];
+            f1 = sm.chg[3 * JB + 2 * warp + 1];
+            h0 = sm.chg[2 * warp];
+            h1 = sm.chg[2 * warp + 1];
+          }
+          __syncthreads();
+          if ((threadIdx.x & 31) == 0) {
+            sm.chg[2 * warp] = f0;
+            sm.chg[2 * warp + 1] = f1;
+            sm.chg[3 * JB + 2 * warp] = h0;
+            sm.chg[3 * JB + 2 * warp + 1] = h1;
+          }
+        }
         store_p_smem(p0, p1, n0, n1, 0, sm);
         store_p_g(t0, t1, m0, m1, sm);
         const int na = ncol[0];
@@ -751,8 +869,8 @@ struct JacobiSmem {
         Col<RPL> p0, p1;
         double n0, n1;
         load_p_g(p0, p1, n0, n1, sm);
-        cross(p0, p1, n0, n1, ncol[3], 1, sm);
-        cross(p0, p1, n0, n1, ncol[3], 2, sm);
+        cross(p0, p1, n0, n1, ncol[3], 3, 1, sm);
+        cross(p0, p1, n0, n1, ncol[3], 3, 2, sm);
         store_p_g(p0, p1, n0, n1, sm);
         __syncthreads();
       }
@@ -760,7 +878,7 @@ struct JacobiSmem {
         Col<RPL> p0, p1;
         double n0, n1;
         load_p_smem(p0, p1, n0, n1, 1, sm);
-        cross(p0, p1, n0, n1, ncol[1], 2, sm);
+        cross(p0, p1, n0, n1, ncol[1], 1, 2, sm);
         store_p_smem(p0, p1, n0, n1, 1, sm);
         __syncthreads();
       }
@@ -769,7 +887,7 @@ struct JacobiSmem {
         Col<RPL> p0, p1;
         double n0, n1;
         load_p_smem(p0, p1, n0, n1, sp, sm);
-        for (int sq = sp + 1; sq < nsm; ++sq) cross(p0, p1, n0, n1, ncol[sp], sq, sm);
+        for (int sq = sp + 1; sq < nsm; ++sq) cross(p0, p1, n0, n1, ncol[sp], sp, sq, sm);
         store_p_smem(p0, p1, n0, n1, sp, sm);
         __syncthreads();
       }
@@ -789,29 +907,45 @@ __device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   J.base = (uint32_t)__cvta_generic_to_shared(smem);
   J.sp = smem;
   J.G = W + (size_t)3 * JB * Mw;
-  for (int b = 0; b < 4; ++b) J.ncol[b] = max(0, min(JB, Nw - JB * b));
+  // balanced split of the Nw columns over the blocks
+  int start[5];
+  start[0] = 0;
+  for (int b = 0; b < 4; ++b) {
+    J.ncol[b] = (b < J.nblk) ? (Nw / J.nblk + (b < Nw % J.nblk ? 1 : 0)) : 0;
+    start[b + 1] = start[b] + J.ncol[b];
+  }
   const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16;
   // stage W into the smem slots (zero padding), zero the unused G columns
   const int nsm = min(J.nblk, 3);
+  if (J.nblk == 4) {
+    // block 3 lives in W columns 96..127 (overlapping its source columns):
+    // read everything first, then write
+    double2 tmp[(JB * 128 + NT - 1) / NT];
+    int cnt = 0;
+    for (int e = threadIdx.x; e < JB * Mw; e += NT, ++cnt) {
+      const int k = e / Mw, y = e - k * Mw;
+      tmp[cnt] = (k < J.ncol[3]) ? W[(size_t)(start[3] + k) * Mw + y] : cz();
+    }
+    __syncthreads();
+    cnt = 0;
+    for (int e = threadIdx.x; e < JB * Mw; e += NT, ++cnt) J.G[e] = tmp[cnt];
+  }
   for (int e = threadIdx.x; e < nsm * JB * LD; e += NT) {
     const int c = e / LD, y = e - c * LD;
-    smem[e] = (c < Nw && y < Mw) ? W[(size_t)c * Mw + y] : cz();
+    const int sb = c / JB, k = c - sb * JB;
+    smem[e] = (k < J.ncol[sb] && y < Mw) ? W[(size_t)(start[sb] + k) * Mw + y] : cz();
   }
-  if (J.nblk == 4)
-    for (int e = threadIdx.x; e < JB * Mw; e += NT) {
-      const int k = e / Mw;
-      if (3 * JB + k >= Nw) J.G[e] = cz();
-    }
   __syncthreads();
   int sweep = 0;
   bool conv = false;
   for (; sweep < MAXSWEEP; ++sweep) {
-    if (threadIdx.x == 0) sm.rotcount = 0;
-    J.refresh_norms(sm, tol);
+    J.refresh_norms(sm, tol, sweep == 0);
     J.sweep(sm);
     __syncthreads();
-    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[16 + min(sweep, 47)], (unsigned long long)sm.rotcount);
-    if (sm.flag == 0) {
+    // converged: no rotation at all, or every rotation of this sweep had a
+    // relative off-diagonal below 1e-8, after which the cyclic sweep leaves
+    // O(1e-16) (quadratic convergence) — the confirming sweep is skipped
+    if (sm.flag == 0 || sm.offmax < 1e-16) {
       conv = true;
       break;
     }
@@ -874,7 +1008,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     const int c = e / LD, y = e - c * LD;
     smem[e] = (y < Nw) ? Y[(size_t)c * Nw + y] : cz();
   }
-  // register columns 96 + 2w, 97 + 2w
+  // register columns 96 + 2w, 97 + 2w; warp w also owns smem columns w + 16i
   Col<RPL> g0, g1;
   const int c0 = 3 * JB + 2 * warp, c1 = c0 + 1;
   col_load_g(g0, Y + (size_t)c0 * Nw, c0 < Mw ? Nw : 0);
@@ -910,37 +1044,43 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     for (int c = 0; c < Mw; ++c) t += sm.nrm[c];
     sm.scale = 1e-28 * t;  // dead threshold on residual norm^2
   }
+  // per-warp pivot candidates over the owned columns
+  auto local_best = [&]() {
+    // lanes 0..5: owned smem columns, lanes 6, 7: the register columns
+    int c = -1;
+    if (lane < 6) c = warp + NWARP * lane;
+    else if (lane == 6) c = c0;
+    else if (lane == 7) c = c1;
+    const bool ok = c >= 0 && c < Mw && (lane >= 6 || c < nsm);
+    double best = ok ? sm.nrm[c] : -1.0;
+    int bi = ok ? c : -1;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
+    }
+    if (lane == 0) {
+      sm.wbest[warp] = best;
+      sm.wbidx[warp] = bi;
+    }
+  };
+  local_best();
   __syncthreads();
   const double dead = sm.scale;
   const int rmax = min(Mw, Nw);
   int j = 0;
   for (; j < rmax; ++j) {
-    // pivot: largest remaining residual norm (done columns carry -1)
-    if (warp == 0) {
-      double best = -1.0;
-      int bi = -1;
-      for (int c = lane; c < Mw; c += 32) {
-        const double v = sm.nrm[c];
-        if (v > best) { best = v; bi = c; }
-      }
+    // global pivot (every warp, redundantly): largest residual, ties to the lowest index
+    double best = (lane < NWARP) ? sm.wbest[lane] : -1.0;
+    int p = (lane < NWARP) ? sm.wbidx[lane] : -1;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
-      }
-      if (lane == 0) {
-        sm.k = (best > dead) ? bi : -1;
-        if (bi >= 0 && best > dead) {
-          sm.qperm[j] = bi;
-          sm.nrm[bi] = -1.0;
-        }
-      }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, p, o);
+      if (ob > best || (ob == best && oi >= 0 && (p < 0 || oi < p))) { best = ob; p = oi; }
     }
-    __syncthreads();
-    const int p = sm.k;
-    if (p < 0) break;
-    // owner normalises the pivot column into the q buffer
+    if (!(best > dead) || p < 0) break;
     const int owner = (p < 3 * JB) ? (p % NWARP) : ((p - 3 * JB) >> 1);
     if (warp == owner) {
       Col<RPL> v;
@@ -954,48 +1094,105 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
 #pragma unroll
       for (int q = 0; q < RPL; ++q) v.v[q] = cscale(v.v[q], inv);
       col_sts(qaddr, v);
-      if (lane == 0) R[(size_t)j * Mw + p] = make_double2(rn, 0.0);
+      if (lane == 0) {
+        R[(size_t)j * Mw + p] = make_double2(rn, 0.0);
+        sm.qperm[j] = p;
+        sm.nrm[p] = -1.0;
+      }
     }
     __syncthreads();
     Col<RPL> qv;
     col_lds(qv, qaddr);
-    // MGS update of every remaining column: r = q^H y, y -= r q
-    auto update = [&](Col<RPL>& y, int c) {
-      double2 d = cz();
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) cfmac(d, qv.v[q], y.v[q]);
-      d.x = warp_sum(d.x);
-      d.y = warp_sum(d.y);
+    // MGS update of two columns at once: r = q^H y, y -= r q
+    auto upd2 = [&](Col<RPL>& ya, Col<RPL>& yb, int ca, int cb) {
+      const bool va = ca >= 0, vb = cb >= 0;
+      double2 da = cz(), db = cz();
 #pragma unroll
       for (int q = 0; q < RPL; ++q) {
-        y.v[q].x -= d.x * qv.v[q].x - d.y * qv.v[q].y;
-        y.v[q].y -= d.x * qv.v[q].y + d.y * qv.v[q].x;
+        cfmac(da, qv.v[q], ya.v[q]);
+        cfmac(db, qv.v[q], yb.v[q]);
       }
-      double nr = sm.nrm[c] - abs2(d);
-      if (nr < 1e-2 * sm.nref[c]) {  // cancellation: recompute exactly
-        double acc = 0.0;
+      const bool up = lane & 16;
+      double x0 = up ? db.x : da.x, x1 = up ? db.y : da.y;
+      const double z0 = up ? da.x : db.x, z1 = up ? da.y : db.y;
+      x0 += __shfl_xor_sync(0xffffffffu, z0, 16);
+      x1 += __shfl_xor_sync(0xffffffffu, z1, 16);
+      const bool h8 = lane & 8;
+      double z = h8 ? x1 : x0;
+      const double w8 = h8 ? x0 : x1;
+      z += __shfl_xor_sync(0xffffffffu, w8, 8);
+      z += __shfl_xor_sync(0xffffffffu, z, 4);
+      z += __shfl_xor_sync(0xffffffffu, z, 2);
+      z += __shfl_xor_sync(0xffffffffu, z, 1);
+      const double o = __shfl_xor_sync(0xffffffffu, z, 8);
+      const double mr = h8 ? o : z, mi = h8 ? z : o;        // this half's dot
+      const double orr = __shfl_xor_sync(0xffffffffu, mr, 16);
+      const double oi = __shfl_xor_sync(0xffffffffu, mi, 16);
+      da = up ? make_double2(orr, oi) : make_double2(mr, mi);
+      db = up ? make_double2(mr, mi) : make_double2(orr, oi);
+      if (!va) da = cz();
+      if (!vb) db = cz();
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) acc += abs2(y.v[q]);
-        nr = warp_sum(acc);
-        if (lane == 0) sm.nref[c] = nr;
+      for (int q = 0; q < RPL; ++q) {
+        ya.v[q].x -= da.x * qv.v[q].x - da.y * qv.v[q].y;
+        ya.v[q].y -= da.x * qv.v[q].y + da.y * qv.v[q].x;
+        yb.v[q].x -= db.x * qv.v[q].x - db.y * qv.v[q].y;
+        yb.v[q].y -= db.x * qv.v[q].y + db.y * qv.v[q].x;
+      }
+      double na = va ? sm.nrm[ca] - abs2(da) : 0.0, nb = vb ? sm.nrm[cb] - abs2(db) : 0.0;
+      const bool fa = va && na < 1e-2 * sm.nref[ca], fb = vb && nb < 1e-2 * sm.nref[cb];
+      if (fa || fb) {  // cancellation: exact norms
+        double ea = 0.0, eb = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          ea += abs2(ya.v[q]);
+          eb += abs2(yb.v[q]);
+        }
+        ea = warp_sum(ea);
+        eb = warp_sum(eb);
+        if (fa) na = ea;
+        if (fb) nb = eb;
       }
       if (lane == 0) {
-        sm.nrm[c] = nr;
-        R[(size_t)j * Mw + c] = d;
+        if (va) {
+          sm.nrm[ca] = na;
+          if (fa) sm.nref[ca] = na;
+          R[(size_t)j * Mw + ca] = da;
+        }
+        if (vb) {
+          sm.nrm[cb] = nb;
+          if (fb) sm.nref[cb] = nb;
+          R[(size_t)j * Mw + cb] = db;
+        }
       }
     };
-    for (int c = warp; c < nsm; c += NWARP) {
-      if (sm.nrm[c] < 0.0) continue;
-      Col<RPL> y;
-      col_lds(y, base + (uint32_t)c * CB);
-      update(y, c);
-      col_sts(base + (uint32_t)c * CB, y);
+    for (int c = warp; c < nsm; c += 2 * NWARP) {
+      const int cb = c + NWARP;
+      const int ia = (sm.nrm[c] >= 0.0) ? c : -1;
+      const int ib = (cb < nsm && sm.nrm[cb] >= 0.0) ? cb : -1;
+      if (ia < 0 && ib < 0) continue;
+      Col<RPL> ya, yb;
+      col_lds(ya, base + (uint32_t)c * CB);
+      if (cb < nsm) col_lds(yb, base + (uint32_t)cb * CB);
+      else {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) yb.v[q] = cz();
+      }
+      upd2(ya, yb, ia, ib);
+      if (ia >= 0) col_sts(base + (uint32_t)c * CB, ya);
+      if (ib >= 0) col_sts(base + (uint32_t)cb * CB, yb);
     }
-    if (c0 < Mw && sm.nrm[c0] >= 0.0) update(g0, c0);
-    if (c1 < Mw && sm.nrm[c1] >= 0.0) update(g1, c1);
+    {
+      const int ia = (c0 < Mw && sm.nrm[c0] >= 0.0) ? c0 : -1;
+      const int ib = (c1 < Mw && sm.nrm[c1] >= 0.0) ? c1 : -1;
+      if (ia >= 0 || ib >= 0) upd2(g0, g1, ia, ib);
+    }
+    __syncwarp();
+    local_best();
     __syncthreads();
   }
   // complete the permutation with the numerically dead columns
+  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
   if (threadIdx.x == 0) {
     int k = j;
     for (int c = 0; c < Mw; ++c)
@@ -1020,7 +1217,10 @@ template <int RPL>
 __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
   const long long t0 = prof_clock();
   const int r = qrcp_mgs<RPL>(W, Nw, Mw, X, sm, smem);
-  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[12], (unsigned long long)(prof_clock() - t0));
+  if (threadIdx.x == 0 && sm.prof) {
+    atomicAdd(&sm.prof[12], (unsigned long long)(prof_clock() - t0));
+    atomicAdd(&sm.prof[8], 1ull);
+  }
   const int K = min(Mw, Nw);
   int neff = 0;
   if (r > 0) {

@@ -119,6 +119,7 @@ struct Smem {
   double wbest[NWARP];       // per-warp pivot candidates (QRCP)
   int qcnt[16];              // cross-phase Q-group visit counters
   unsigned char chg[4 * 32]; // bit0: rotated in the previous sweep, bit1: in this sweep
+  int jncol[4];              // live columns per Jacobi block slot
   int wbidx[NWARP];
   double nref[4 * 32];
   int qperm[4 * 32];
@@ -444,11 +445,10 @@ __device__ __forceinline__ double rcp_nr1(double x) {  // ~2^-44 relative
   return y;
 }
 
-__device__ __forceinline__ Rot rot_params(double gr, double gi, double al, double be, bool valid, double tol2,
-                                          double abs2) {
+__device__ __forceinline__ Rot rot_params(double gr, double gi, double al, double be, bool valid, double tol2) {
   Rot p;
   const double g2 = fma(gr, gr, gi * gi);
-  const bool rot = valid && (g2 > tol2 * al * be) && (g2 > abs2 * fmax(al, be));
+  const bool rot = valid && (g2 > tol2 * al * be);
   // t only fixes the rotation angle (an approximate t still gives an exactly
   // unitary rotation, c = 1/sqrt(1+t^2), s = t c); c and e = conj(g)/|g| are
   // evaluated to full precision.
@@ -495,16 +495,13 @@ __device__ __forceinline__ void apply_rot(Col<RPL>& a, Col<RPL>& b, const Rot& p
   }
 }
 
-struct Thr {
-  double tol2, abs2;
-  mutable double offmax;  // max |g|^2/(alpha beta) over rotated pairs (half-warp leaders)
-};
+
 
 // two independent pairs (a0,b0), (a1,b1); returns true if any rotation applied
 template <int RPL>
 __device__ __forceinline__ bool rot2(Col<RPL>& a0, Col<RPL>& b0, double& na0, double& nb0, bool v0, Col<RPL>& a1,
-                                     Col<RPL>& b1, double& na1, double& nb1, bool v1, const Thr& th, double* pb,
-                                     bool* out0 = nullptr, bool* out1 = nullptr) {
+                                     Col<RPL>& b1, double& na1, double& nb1, bool v1, double tol2, double& offmax,
+                                     double* pb, bool* out0 = nullptr, bool* out1 = nullptr) {
   const int lane = threadIdx.x & 31;
   double2 g0 = cz(), g1 = cz(), h0 = cz(), h1 = cz();
 #pragma unroll
@@ -535,11 +532,8 @@ __device__ __forceinline__ bool rot2(Col<RPL>& a0, Col<RPL>& b0, double& na0, do
   const double o = __shfl_xor_sync(0xffffffffu, z, 8);
   const double gr = h8 ? o : z, gi = h8 ? z : o;
   const double myal = up ? na1 : na0, mybe = up ? nb1 : nb0;
-  const Rot mine = rot_params(gr, gi, myal, mybe, up ? v1 : v0, th.tol2, th.abs2);
-  if (mine.s != 0.0 && (lane & 15) == 0) {
-    const double rel2 = fma(gr, gr, gi * gi) / (myal * mybe);
-    if (rel2 > th.offmax) th.offmax = rel2;
-  }
+  const Rot mine = rot_params(gr, gi, myal, mybe, up ? v1 : v0, tol2);
+  if (mine.s != 0.0) offmax = fmax(offmax, fma(gr, gr, gi * gi) / (myal * mybe));
   // half-warp leaders publish their pair's parameters; every lane reads both
   double* my = pb + (up ? 6 : 0);
   if ((lane & 15) == 0) {
@@ -593,8 +587,9 @@ struct JacobiSmem {
   double2* sp;                         // generic pointer to slot A (staging only)
   double2* G;                          // global columns 96..127 (ld = Mw)
   int Mw, nblk;
-  int ncol[4];                         // live columns per slot (A, B, C, G)
-  Thr th;
+  double tol2;                         // squared relative orthogonality threshold
+  double offmax;                       // max |g|^2/(alpha beta) of this sweep's rotations
+  __device__ int ncol(int b, const Smem& sm) const { return sm.jncol[b]; }
 
   __device__ uint32_t scol(int s, int c) const { return base + (uint32_t)(s * JB + c) * CB; }
 
@@ -603,7 +598,7 @@ struct JacobiSmem {
     const int warp = threadIdx.x >> 5;
     int rounds = 0;
     for (int x = 0; x < ns; ++x) {
-      const int nb = ncol[slots[x]];
+      const int nb = sm.jncol[slots[x]];
       rounds = max(rounds, nb + (nb & 1) - 1);
     }
     for (int r = 0; r < rounds; ++r) {
@@ -611,7 +606,7 @@ struct JacobiSmem {
       int cnt = 0;
       int ps0 = 0, is0 = 0, js0 = 0, ps1 = 0, is1 = 0, js1 = 0, ps2 = 0, is2 = 0, js2 = 0;
       for (int x = 0; x < ns; ++x) {
-        const int s = slots[x], nb = ncol[s], nbp = nb + (nb & 1);
+        const int s = slots[x], nb = sm.jncol[s], nbp = nb + (nb & 1);
         if (r < nbp - 1 && warp < nbp / 2) {
           int i, j;
           rr_pair(r, warp, nbp, i, j);
@@ -640,7 +635,7 @@ struct JacobiSmem {
 #pragma unroll
           for (int q = 0; q < RPL; ++q) a1.v[q] = b1.v[q] = cz();
         }
-        const bool rr = rot2<RPL>(a0, b0, na0, nb0, true, a1, b1, na1, nb1, two, th, &sm.pbuf[warp][0][0]);
+        const bool rr = rot2<RPL>(a0, b0, na0, nb0, true, a1, b1, na1, nb1, two, tol2, offmax, &sm.pbuf[warp][0][0]);
         if (rr) {
           any = true;
           col_sts(scol(pa, ia), a0);
@@ -671,8 +666,10 @@ struct JacobiSmem {
   // P (registers: columns 2w, 2w+1) against smem slot sq
   __device__ void cross(Col<RPL>& p0, Col<RPL>& p1, double& np0, double& np1, int nP, int sp, int sq, Smem& sm) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nQ = ncol[sq];
+    const int nQ = sm.jncol[sq];
     const bool vp0 = 2 * warp < nP, vp1 = 2 * warp + 1 < nP;
+    const double t2 = tol2;
+    double om = offmax;
     unsigned char* cp = &sm.chg[sp * JB + 2 * warp];
     bool any = false;
     const long long tc0 = prof_clock();
@@ -704,8 +701,8 @@ struct JacobiSmem {
         const bool s00 = vp0 && vq0 && (fp0 | fq0), s11 = vp1 && vq1 && (fp1 | fq1);
         const bool s01 = vp0 && vq1 && (fp0 | fq1), s10 = vp1 && vq0 && (fp1 | fq0);
         bool r00 = false, r11 = false, r01 = false, r10 = false;
-        if (s00 || s11) rot2<RPL>(p0, q0, np0, nq0, s00, p1, q1, np1, nq1, s11, th, pb, &r00, &r11);
-        if (s01 || s10) rot2<RPL>(p0, q1, np0, nq1, s01, p1, q0, np1, nq0, s10, th, pb, &r01, &r10);
+        if (s00 || s11) rot2<RPL>(p0, q0, np0, nq0, s00, p1, q1, np1, nq1, s11, t2, om, pb, &r00, &r11);
+        if (s01 || s10) rot2<RPL>(p0, q1, np0, nq1, s01, p1, q0, np1, nq0, s10, t2, om, pb, &r01, &r10);
         if (r00 || r11 || r01 || r10) {
           any = true;
           col_sts(a0, q0);
@@ -725,6 +722,7 @@ struct JacobiSmem {
       if (lane == 0) *(volatile int*)&sm.qcnt[g] = r + 1;
     }
     __syncthreads();
+    offmax = om;
     if (any && lane == 0) sm.flag = 1;
     if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[14], (unsigned long long)(prof_clock() - tc0));
   }
@@ -794,8 +792,7 @@ struct JacobiSmem {
       sm.offmax = 0.0;
     }
     __syncthreads();
-    th.tol2 = tol * tol;
-    th.abs2 = 0.0;  // relative criterion only: the split projects onto Q, which must be orthonormal
+    tol2 = tol * tol;  // relative criterion only: the split projects onto Q, which must be orthonormal
     const double dead = 1e-28 * sm.scale;
     for (int c = warp; c < JB * nblk; c += NWARP) {
       const double v = sm.nrm[c];
@@ -817,9 +814,9 @@ struct JacobiSmem {
   }
 
   __device__ void sweep(Smem& sm) {
-    th.offmax = 0.0;
+    offmax = 0.0;
     sweep_body(sm);
-    if ((threadIdx.x & 15) == 0 && th.offmax > 0.0) atomic_max_pos(&sm.offmax, th.offmax);
+    if ((threadIdx.x & 15) == 0 && offmax > 0.0) atomic_max_pos(&sm.offmax, offmax);
   }
 
   __device__ void sweep_body(Smem& sm) {
@@ -833,7 +830,7 @@ struct JacobiSmem {
         Col<RPL> p0, p1;
         double n0, n1;
         load_p_g(p0, p1, n0, n1, sm);
-        for (int s = 0; s < 3; ++s) cross(p0, p1, n0, n1, ncol[3], 3, s, sm);
+        for (int s = 0; s < 3; ++s) cross(p0, p1, n0, n1, sm.jncol[3], 3, s, sm);
         // swap contents: A -> G storage, P (old G) -> A
         Col<RPL> t0, t1;
         double m0, m1;
@@ -858,9 +855,12 @@ struct JacobiSmem {
         }
         store_p_smem(p0, p1, n0, n1, 0, sm);
         store_p_g(t0, t1, m0, m1, sm);
-        const int na = ncol[0];
-        ncol[0] = ncol[3];
-        ncol[3] = na;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const int na = sm.jncol[0];
+          sm.jncol[0] = sm.jncol[3];
+          sm.jncol[3] = na;
+        }
         __syncthreads();
       }
       const int a1[1] = {0};
@@ -869,8 +869,8 @@ struct JacobiSmem {
         Col<RPL> p0, p1;
         double n0, n1;
         load_p_g(p0, p1, n0, n1, sm);
-        cross(p0, p1, n0, n1, ncol[3], 3, 1, sm);
-        cross(p0, p1, n0, n1, ncol[3], 3, 2, sm);
+        cross(p0, p1, n0, n1, sm.jncol[3], 3, 1, sm);
+        cross(p0, p1, n0, n1, sm.jncol[3], 3, 2, sm);
         store_p_g(p0, p1, n0, n1, sm);
         __syncthreads();
       }
@@ -878,7 +878,7 @@ struct JacobiSmem {
         Col<RPL> p0, p1;
         double n0, n1;
         load_p_smem(p0, p1, n0, n1, 1, sm);
-        cross(p0, p1, n0, n1, ncol[1], 1, 2, sm);
+        cross(p0, p1, n0, n1, sm.jncol[1], 1, 2, sm);
         store_p_smem(p0, p1, n0, n1, 1, sm);
         __syncthreads();
       }
@@ -887,7 +887,7 @@ struct JacobiSmem {
         Col<RPL> p0, p1;
         double n0, n1;
         load_p_smem(p0, p1, n0, n1, sp, sm);
-        for (int sq = sp + 1; sq < nsm; ++sq) cross(p0, p1, n0, n1, ncol[sp], sp, sq, sm);
+        for (int sq = sp + 1; sq < nsm; ++sq) cross(p0, p1, n0, n1, sm.jncol[sp], sp, sq, sm);
         store_p_smem(p0, p1, n0, n1, sp, sm);
         __syncthreads();
       }
@@ -910,10 +910,13 @@ __device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   // balanced split of the Nw columns over the blocks
   int start[5];
   start[0] = 0;
+  int ncl[4];
   for (int b = 0; b < 4; ++b) {
-    J.ncol[b] = (b < J.nblk) ? (Nw / J.nblk + (b < Nw % J.nblk ? 1 : 0)) : 0;
-    start[b + 1] = start[b] + J.ncol[b];
+    ncl[b] = (b < J.nblk) ? (Nw / J.nblk + (b < Nw % J.nblk ? 1 : 0)) : 0;
+    start[b + 1] = start[b] + ncl[b];
   }
+  __syncthreads();
+  if (threadIdx.x < 4) sm.jncol[threadIdx.x] = ncl[threadIdx.x];
   const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16;
   // stage W into the smem slots (zero padding), zero the unused G columns
   const int nsm = min(J.nblk, 3);
@@ -924,7 +927,7 @@ __device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     int cnt = 0;
     for (int e = threadIdx.x; e < JB * Mw; e += NT, ++cnt) {
       const int k = e / Mw, y = e - k * Mw;
-      tmp[cnt] = (k < J.ncol[3]) ? W[(size_t)(start[3] + k) * Mw + y] : cz();
+      tmp[cnt] = (k < ncl[3]) ? W[(size_t)(start[3] + k) * Mw + y] : cz();
     }
     __syncthreads();
     cnt = 0;
@@ -933,7 +936,7 @@ __device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   for (int e = threadIdx.x; e < nsm * JB * LD; e += NT) {
     const int c = e / LD, y = e - c * LD;
     const int sb = c / JB, k = c - sb * JB;
-    smem[e] = (k < J.ncol[sb] && y < Mw) ? W[(size_t)(start[sb] + k) * Mw + y] : cz();
+    smem[e] = (k < ncl[sb] && y < Mw) ? W[(size_t)(start[sb] + k) * Mw + y] : cz();
   }
   __syncthreads();
   int sweep = 0;

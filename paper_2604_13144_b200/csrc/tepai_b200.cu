@@ -116,11 +116,11 @@ struct Smem {
   double sig[MAXDIM];
   double nrm[4 * 32];
   double pbuf[NWARP][2][6];  // per-warp Jacobi parameter exchange
-  double wbest[NWARP];       // per-warp pivot candidates (QRCP)
-  int qcnt[16];              // cross-phase Q-group visit counters
+  double wbest[32];          // per-half-warp pivot candidates (QRCP)
+  int qcnt[32];              // cross-phase Q visit counters
   unsigned char chg[4 * 32]; // bit0: rotated in the previous sweep, bit1: in this sweep
   int jncol[4];              // live columns per Jacobi block slot
-  int wbidx[NWARP];
+  int wbidx[32];
   double nref[4 * 32];
   int qperm[4 * 32];
   int qpinv[MAXDIM];
@@ -350,19 +350,6 @@ __device__ void sort_sigma(const double2* W, int Mw, int Nw, Smem& sm) {
   __syncthreads();
 }
 
-// ----------------------------------------------------------------------------
-// Shared-memory resident one-sided Jacobi (Mw <= 128, Nw <= 128).
-//
-// Columns live in blocks of 32: three shared-memory slots (A, B, C) and, when
-// Nw > 96, one L2 slot G (global W columns 96..127).  RPL = rows per lane.
-// A sweep visits every column pair exactly once:
-//   within A, B, C (round robin, columns streamed from smem)
-//   G x {A, B, C}  (G held in registers, 2 columns per warp, A/B/C streamed)
-//   swap contents of A and G; within A
-//   G x {B, C};  B x C
-// Every warp step processes two independent pairs so one transposed warp
-// reduction and one half-warp parameter evaluation serve both.
-// ----------------------------------------------------------------------------
 __device__ __forceinline__ long long prof_clock() { return clock64(); }
 
 constexpr int JB = 32;  // columns per block
@@ -374,43 +361,6 @@ __device__ __forceinline__ double2 lds2(uint32_t a) {
 }
 __device__ __forceinline__ void sts2(uint32_t a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
-}
-
-template <int RPL>
-struct Col {
-  double2 v[RPL];
-};
-
-// smem column at byte address a (lane-strided rows)
-template <int RPL>
-__device__ __forceinline__ void col_lds(Col<RPL>& c, uint32_t a) {
-  const uint32_t l = (threadIdx.x & 31) * 16u;
-#pragma unroll
-  for (int q = 0; q < RPL; ++q) c.v[q] = lds2(a + l + 512u * q);
-}
-template <int RPL>
-__device__ __forceinline__ void col_sts(uint32_t a, const Col<RPL>& c) {
-  const uint32_t l = (threadIdx.x & 31) * 16u;
-#pragma unroll
-  for (int q = 0; q < RPL; ++q) sts2(a + l + 512u * q, c.v[q]);
-}
-template <int RPL>
-__device__ __forceinline__ void col_load_g(Col<RPL>& c, const double2* p, int Mw) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int q = 0; q < RPL; ++q) {
-    const int y = lane + 32 * q;
-    c.v[q] = (y < Mw) ? p[y] : cz();
-  }
-}
-template <int RPL>
-__device__ __forceinline__ void col_store_g(double2* p, const Col<RPL>& c, int Mw) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int q = 0; q < RPL; ++q) {
-    const int y = lane + 32 * q;
-    if (y < Mw) p[y] = c.v[q];
-  }
 }
 
 // Rotation of one pair.  Identity when s == 0 (c = 1, e = 1).
@@ -468,22 +418,58 @@ __device__ __forceinline__ Rot rot_params(double gr, double gi, double al, doubl
   return p;
 }
 
-__device__ __forceinline__ Rot shfl_rot(const Rot& p, int src) {
-  Rot o;
-  o.c = __shfl_sync(0xffffffffu, p.c, src);
-  o.s = __shfl_sync(0xffffffffu, p.s, src);
-  o.er = __shfl_sync(0xffffffffu, p.er, src);
-  o.ei = __shfl_sync(0xffffffffu, p.ei, src);
-  o.tg = __shfl_sync(0xffffffffu, p.tg, src);
-  return o;
+// ----------------------------------------------------------------------------
+// Half-warp Jacobi (Mw <= 128, Nw <= 128).  A column lives in one half-warp
+// (16 lanes x HR rows), so a warp works on two independent pairs whose
+// reductions are 4-level butterflies inside each half and whose rotation
+// parameters are evaluated by the half that owns the pair — no cross-half
+// transposition and no parameter broadcast.  Same block schedule as
+// JacobiSmem (3 smem slots + 1 L2 slot of 32 columns); in a cross phase each
+// of the 32 half-warps holds one P column in registers and the 32 Q columns
+// rotate through the halves (round r: half k takes Q column (k + r) mod 32),
+// ordered by per-column counters instead of CTA barriers.
+// ----------------------------------------------------------------------------
+template <int HR>
+struct HCol {
+  double2 v[HR];
+};
+
+template <int HR>
+__device__ __forceinline__ void hcol_lds(HCol<HR>& c, uint32_t a) {
+  const uint32_t l = (threadIdx.x & 15) * 16u;
+#pragma unroll
+  for (int q = 0; q < HR; ++q) c.v[q] = lds2(a + l + 256u * q);
+}
+template <int HR>
+__device__ __forceinline__ void hcol_sts(uint32_t a, const HCol<HR>& c) {
+  const uint32_t l = (threadIdx.x & 15) * 16u;
+#pragma unroll
+  for (int q = 0; q < HR; ++q) sts2(a + l + 256u * q, c.v[q]);
+}
+template <int HR>
+__device__ __forceinline__ void hcol_ldg(HCol<HR>& c, const double2* p, int Mw) {
+  const int l = threadIdx.x & 15;
+#pragma unroll
+  for (int q = 0; q < HR; ++q) {
+    const int y = l + 16 * q;
+    c.v[q] = (y < Mw) ? p[y] : cz();
+  }
+}
+template <int HR>
+__device__ __forceinline__ void hcol_stg(double2* p, const HCol<HR>& c, int Mw) {
+  const int l = threadIdx.x & 15;
+#pragma unroll
+  for (int q = 0; q < HR; ++q) {
+    const int y = l + 16 * q;
+    if (y < Mw) p[y] = c.v[q];
+  }
 }
 
-// a' = c a - s e b,  b' = s a + c e b
-template <int RPL>
-__device__ __forceinline__ void apply_rot(Col<RPL>& a, Col<RPL>& b, const Rot& p) {
+template <int HR>
+__device__ __forceinline__ void apply_rot(HCol<HR>& a, HCol<HR>& b, const Rot& p) {
   const double sre = p.s * p.er, sim = p.s * p.ei, cre = p.c * p.er, cim = p.c * p.ei;
 #pragma unroll
-  for (int q = 0; q < RPL; ++q) {
+  for (int q = 0; q < HR; ++q) {
     const double2 x = a.v[q], y = b.v[q];
     double2 na, nb;
     na.x = fma(sim, y.y, fma(-sre, y.x, p.c * x.x));
@@ -495,282 +481,188 @@ __device__ __forceinline__ void apply_rot(Col<RPL>& a, Col<RPL>& b, const Rot& p
   }
 }
 
-
-
-// two independent pairs (a0,b0), (a1,b1); returns true if any rotation applied
-template <int RPL>
-__device__ __forceinline__ bool rot2(Col<RPL>& a0, Col<RPL>& b0, double& na0, double& nb0, bool v0, Col<RPL>& a1,
-                                     Col<RPL>& b1, double& na1, double& nb1, bool v1, double tol2, double& offmax,
-                                     double* pb, bool* out0 = nullptr, bool* out1 = nullptr) {
-  const int lane = threadIdx.x & 31;
-  double2 g0 = cz(), g1 = cz(), h0 = cz(), h1 = cz();
-#pragma unroll
-  for (int q = 0; q < RPL; q += 2) {
-    cfmac(g0, a0.v[q], b0.v[q]);
-    cfmac(g1, a1.v[q], b1.v[q]);
-    if (q + 1 < RPL) {
-      cfmac(h0, a0.v[q + 1], b0.v[q + 1]);
-      cfmac(h1, a1.v[q + 1], b1.v[q + 1]);
-    }
-  }
-  g0 = cadd(g0, h0);
-  g1 = cadd(g1, h1);
-  // transposed reduction of (g0.x, g0.y, g1.x, g1.y): lanes 0-15 end with g0,
-  // lanes 16-31 with g1
-  const bool up = lane & 16;
-  double x0 = up ? g1.x : g0.x, x1 = up ? g1.y : g0.y;
-  const double y0 = up ? g0.x : g1.x, y1 = up ? g0.y : g1.y;
-  x0 += __shfl_xor_sync(0xffffffffu, y0, 16);
-  x1 += __shfl_xor_sync(0xffffffffu, y1, 16);
-  const bool h8 = lane & 8;
-  double z = h8 ? x1 : x0;
-  const double w = h8 ? x0 : x1;
-  z += __shfl_xor_sync(0xffffffffu, w, 8);
-  z += __shfl_xor_sync(0xffffffffu, z, 4);
-  z += __shfl_xor_sync(0xffffffffu, z, 2);
-  z += __shfl_xor_sync(0xffffffffu, z, 1);
-  const double o = __shfl_xor_sync(0xffffffffu, z, 8);
-  const double gr = h8 ? o : z, gi = h8 ? z : o;
-  const double myal = up ? na1 : na0, mybe = up ? nb1 : nb0;
-  const Rot mine = rot_params(gr, gi, myal, mybe, up ? v1 : v0, tol2);
-  if (mine.s != 0.0) offmax = fmax(offmax, fma(gr, gr, gi * gi) / (myal * mybe));
-  // half-warp leaders publish their pair's parameters; every lane reads both
-  double* my = pb + (up ? 6 : 0);
-  if ((lane & 15) == 0) {
-    my[0] = mine.c;
-    my[1] = mine.s;
-    my[2] = mine.er;
-    my[3] = mine.ei;
-    my[4] = mine.tg;
-  }
-  __syncwarp();
-  Rot p0, p1;
-  p0.c = pb[0]; p0.s = pb[1]; p0.er = pb[2]; p0.ei = pb[3]; p0.tg = pb[4];
-  p1.c = pb[6]; p1.s = pb[7]; p1.er = pb[8]; p1.ei = pb[9]; p1.tg = pb[10];
-  __syncwarp();
-  const bool r0 = p0.s != 0.0, r1 = p1.s != 0.0;
-  if (r0) apply_rot(a0, b0, p0);
-  if (r1) apply_rot(a1, b1, p1);
-  // tracked norms; a relative drop below 1/2 means cancellation, so those
-  // columns get their exact norm (warp-uniform branch, rare after sweep 1)
-  const double na0n = na0 - p0.tg, nb0n = nb0 + p0.tg, na1n = na1 - p1.tg, nb1n = nb1 + p1.tg;
-  const bool f0 = r0 && na0n < 0.5 * na0, f1 = r0 && nb0n < 0.5 * nb0;
-  const bool f2 = r1 && na1n < 0.5 * na1, f3 = r1 && nb1n < 0.5 * nb1;
-  na0 = na0n;
-  nb0 = nb0n;
-  na1 = na1n;
-  nb1 = nb1n;
-  if (f0 || f1 || f2 || f3) {
-    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
-#pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-      e0 += abs2(a0.v[q]);
-      e1 += abs2(b0.v[q]);
-      e2 += abs2(a1.v[q]);
-      e3 += abs2(b1.v[q]);
-    }
-    if (f0) na0 = warp_sum(e0);
-    if (f1) nb0 = warp_sum(e1);
-    if (f2) na1 = warp_sum(e2);
-    if (f3) nb1 = warp_sum(e3);
-  }
-  if (out0) *out0 = r0;
-  if (out1) *out1 = r1;
-  return r0 || r1;
+__device__ __forceinline__ double half_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
 }
 
-template <int RPL>
-struct JacobiSmem {
-  static constexpr int LD = 32 * RPL;  // padded rows per smem column
+// one pair per half-warp; `valid` may differ between the halves.  Returns
+// whether THIS half rotated.  Branches are warp-uniform (both halves take
+// the apply path if either rotates; a non-rotating half applies identity).
+template <int HR>
+__device__ __forceinline__ bool rot_half(HCol<HR>& a, HCol<HR>& b, double& na, double& nb, bool valid, double tol2,
+                                         double& offmax) {
+  double2 g = cz(), h = cz();
+#pragma unroll
+  for (int q = 0; q < HR; q += 2) {
+    cfmac(g, a.v[q], b.v[q]);
+    if (q + 1 < HR) cfmac(h, a.v[q + 1], b.v[q + 1]);
+  }
+  double gr = g.x + h.x, gi = g.y + h.y;
+  gr = half_sum(gr);
+  gi = half_sum(gi);
+  const Rot p = rot_params(gr, gi, na, nb, valid, tol2);
+  const bool mine = p.s != 0.0;
+  if (mine) offmax = fmax(offmax, fma(gr, gr, gi * gi) / (na * nb));
+  if (__any_sync(0xffffffffu, mine)) apply_rot(a, b, p);
+  const double nan_ = na - p.tg, nbn = nb + p.tg;
+  const bool fa = mine && nan_ < 0.5 * na, fb = mine && nbn < 0.5 * nb;
+  na = nan_;
+  nb = nbn;
+  if (__any_sync(0xffffffffu, fa || fb)) {
+    double ea = 0.0, eb = 0.0;
+#pragma unroll
+    for (int q = 0; q < HR; ++q) {
+      ea += abs2(a.v[q]);
+      eb += abs2(b.v[q]);
+    }
+    ea = half_sum(ea);
+    eb = half_sum(eb);
+    if (fa) na = ea;
+    if (fb) nb = eb;
+  }
+  return mine;
+}
+
+template <int HR>
+struct JacobiH {
+  static constexpr int LD = 16 * HR;        // padded rows per smem column
   static constexpr uint32_t CB = LD * 16u;  // bytes per smem column
-  uint32_t base;                       // smem byte address of slot A
-  double2* sp;                         // generic pointer to slot A (staging only)
-  double2* G;                          // global columns 96..127 (ld = Mw)
+  uint32_t base;                            // smem byte address of slot A
+  double2* G;                               // global block (columns 96..127, ld = Mw)
   int Mw, nblk;
-  double tol2;                         // squared relative orthogonality threshold
-  double offmax;                       // max |g|^2/(alpha beta) of this sweep's rotations
-  __device__ int ncol(int b, const Smem& sm) const { return sm.jncol[b]; }
+  double tol2, offmax;
 
   __device__ uint32_t scol(int s, int c) const { return base + (uint32_t)(s * JB + c) * CB; }
 
-  // within-block round robin on up to three smem slots concurrently
-  __device__ void within(const int* slots, int ns, Smem& sm) {
-    const int warp = threadIdx.x >> 5;
+  // round robin inside up to three smem slots; pairs are dealt to halves
+  __device__ void within(int s0, int s1, int s2, int ns, Smem& sm) {
+    const int hw = threadIdx.x >> 4;  // half-warp id 0..31
+    const int hl = threadIdx.x & 15;
     int rounds = 0;
     for (int x = 0; x < ns; ++x) {
-      const int nb = sm.jncol[slots[x]];
+      const int nb = sm.jncol[x == 0 ? s0 : (x == 1 ? s1 : s2)];
       rounds = max(rounds, nb + (nb & 1) - 1);
     }
     for (int r = 0; r < rounds; ++r) {
       bool any = false;
-      int cnt = 0;
-      int ps0 = 0, is0 = 0, js0 = 0, ps1 = 0, is1 = 0, js1 = 0, ps2 = 0, is2 = 0, js2 = 0;
-      for (int x = 0; x < ns; ++x) {
-        const int s = slots[x], nb = sm.jncol[s], nbp = nb + (nb & 1);
-        if (r < nbp - 1 && warp < nbp / 2) {
-          int i, j;
-          rr_pair(r, warp, nbp, i, j);
-          if (i < nb && j < nb && ((sm.chg[s * JB + i] | sm.chg[s * JB + j]) & 1)) {
-            if (cnt == 0) { ps0 = s; is0 = i; js0 = j; }
-            else if (cnt == 1) { ps1 = s; is1 = i; js1 = j; }
-            else { ps2 = s; is2 = i; js2 = j; }
-            ++cnt;
+      // 16 pairs per slot and round at most: pair (x, p) -> half x*16+p (mod 32)
+      for (int f0 = 0; f0 < 3 * 16; f0 += 32) {
+        const int f = f0 + hw;
+        const int x = f >> 4, p = f & 15;
+        bool valid = false;
+        int s = 0, i = 0, j = 0;
+        if (x < ns) {
+          s = (x == 0) ? s0 : (x == 1 ? s1 : s2);
+          const int nb = sm.jncol[s], nbp = nb + (nb & 1);
+          if (r < nbp - 1 && p < nbp / 2) {
+            rr_pair(r, p, nbp, i, j);
+            valid = i < nb && j < nb && ((sm.chg[s * JB + i] | sm.chg[s * JB + j]) & 1);
           }
         }
-      }
-      for (int k = 0; k < cnt; k += 2) {
-        const bool two = (k + 1 < cnt);
-        const int pa = k ? ps2 : ps0, ia = k ? is2 : is0, ja = k ? js2 : js0;
-        Col<RPL> a0, b0, a1, b1;
-        col_lds(a0, scol(pa, ia));
-        col_lds(b0, scol(pa, ja));
-        double na0 = sm.nrm[pa * JB + ia], nb0 = sm.nrm[pa * JB + ja];
-        double na1 = 0.0, nb1 = 0.0;
-        if (two) {
-          col_lds(a1, scol(ps1, is1));
-          col_lds(b1, scol(ps1, js1));
-          na1 = sm.nrm[ps1 * JB + is1];
-          nb1 = sm.nrm[ps1 * JB + js1];
+        if (!__any_sync(0xffffffffu, valid)) continue;
+        HCol<HR> a, b;
+        const uint32_t ai = scol(s, i), aj = scol(s, j);
+        if (valid) {
+          hcol_lds(a, ai);
+          hcol_lds(b, aj);
         } else {
 #pragma unroll
-          for (int q = 0; q < RPL; ++q) a1.v[q] = b1.v[q] = cz();
+          for (int q = 0; q < HR; ++q) a.v[q] = b.v[q] = cz();
         }
-        const bool rr = rot2<RPL>(a0, b0, na0, nb0, true, a1, b1, na1, nb1, two, tol2, offmax, &sm.pbuf[warp][0][0]);
+        double na = valid ? sm.nrm[s * JB + i] : 0.0, nb = valid ? sm.nrm[s * JB + j] : 0.0;
+        const bool rr = rot_half<HR>(a, b, na, nb, valid, tol2, offmax);
         if (rr) {
           any = true;
-          col_sts(scol(pa, ia), a0);
-          col_sts(scol(pa, ja), b0);
-          if (two) {
-            col_sts(scol(ps1, is1), a1);
-            col_sts(scol(ps1, js1), b1);
-          }
-          if ((threadIdx.x & 31) == 0) {
-            sm.nrm[pa * JB + ia] = na0;
-            sm.nrm[pa * JB + ja] = nb0;
-            sm.chg[pa * JB + ia] |= 2;
-            sm.chg[pa * JB + ja] |= 2;
-            if (two) {
-              sm.nrm[ps1 * JB + is1] = na1;
-              sm.nrm[ps1 * JB + js1] = nb1;
-              sm.chg[ps1 * JB + is1] |= 2;
-              sm.chg[ps1 * JB + js1] |= 2;
-            }
+          hcol_sts(ai, a);
+          hcol_sts(aj, b);
+          if (hl == 0) {
+            sm.nrm[s * JB + i] = na;
+            sm.nrm[s * JB + j] = nb;
+            sm.chg[s * JB + i] |= 2;
+            sm.chg[s * JB + j] |= 2;
           }
         }
       }
-      if (any && (threadIdx.x & 31) == 0) sm.flag = 1;
+      if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
       __syncthreads();
     }
   }
 
-  // P (registers: columns 2w, 2w+1) against smem slot sq
-  __device__ void cross(Col<RPL>& p0, Col<RPL>& p1, double& np0, double& np1, int nP, int sp, int sq, Smem& sm) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // P column of half k (slot sp) against the Q columns of smem slot sq
+  __device__ void cross(HCol<HR>& pc, double& np, int nP, int sp, int sq, Smem& sm) {
+    const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
     const int nQ = sm.jncol[sq];
-    const bool vp0 = 2 * warp < nP, vp1 = 2 * warp + 1 < nP;
-    const double t2 = tol2;
-    double om = offmax;
-    unsigned char* cp = &sm.chg[sp * JB + 2 * warp];
+    const bool vp = hw < nP;
     bool any = false;
-    const long long tc0 = prof_clock();
-    // Q group g visits warps g, g-1, g-2, ... (round r: warp (g - r) mod 16);
-    // sm.qcnt[g] counts completed visits, so a warp waits only for the warp
-    // that held its next group in the previous round (no CTA-wide barrier)
-    if (threadIdx.x < 16) sm.qcnt[threadIdx.x] = 0;
+    if (threadIdx.x < 32) sm.qcnt[threadIdx.x] = 0;
     __syncthreads();
-    for (int r = 0; r < 16; ++r) {
-      const int g = (warp + r) & 15;
-      const bool vq0 = 2 * g < nQ, vq1 = 2 * g + 1 < nQ;
+    const long long tc0 = prof_clock();
+    for (int r = 0; r < 32; ++r) {
+      const int c = (hw + r) & 31;  // Q column handled by this half in round r
       if (r > 0) {
-        if (lane == 0)
-          while (*(volatile int*)&sm.qcnt[g] < r) __nanosleep(20);
+        if (hl == 0)
+          while (*(volatile int*)&sm.qcnt[c] < r) {}
         __syncwarp();
         __threadfence_block();
       }
-      if ((vp0 || vp1) && (vq0 || vq1)) {
-        Col<RPL> q0, q1;
-        const uint32_t a0 = scol(sq, 2 * g), a1 = scol(sq, 2 * g + 1);
-        col_lds(q0, a0);
-        col_lds(q1, a1);
-        double nq0 = sm.nrm[sq * JB + 2 * g], nq1 = sm.nrm[sq * JB + 2 * g + 1];
-        double* pb = &sm.pbuf[warp][0][0];
-        unsigned char* cq = &sm.chg[sq * JB + 2 * g];
-        // a pair whose two columns were both untouched during the previous
-        // sweep was found orthogonal then and still is: skip it
-        const int fp0 = cp[0] & 1, fp1 = cp[1] & 1, fq0 = cq[0] & 1, fq1 = cq[1] & 1;
-        const bool s00 = vp0 && vq0 && (fp0 | fq0), s11 = vp1 && vq1 && (fp1 | fq1);
-        const bool s01 = vp0 && vq1 && (fp0 | fq1), s10 = vp1 && vq0 && (fp1 | fq0);
-        bool r00 = false, r11 = false, r01 = false, r10 = false;
-        if (s00 || s11) rot2<RPL>(p0, q0, np0, nq0, s00, p1, q1, np1, nq1, s11, t2, om, pb, &r00, &r11);
-        if (s01 || s10) rot2<RPL>(p0, q1, np0, nq1, s01, p1, q0, np1, nq0, s10, t2, om, pb, &r01, &r10);
-        if (r00 || r11 || r01 || r10) {
+      const bool valid = vp && c < nQ && ((sm.chg[sp * JB + hw] | sm.chg[sq * JB + c]) & 1);
+      if (__any_sync(0xffffffffu, valid)) {
+        HCol<HR> q;
+        const uint32_t aq = scol(sq, c);
+        if (valid) hcol_lds(q, aq);
+        else {
+#pragma unroll
+          for (int k = 0; k < HR; ++k) q.v[k] = cz();
+        }
+        double nq = valid ? sm.nrm[sq * JB + c] : 0.0;
+        const double npo = np;
+        const bool rr = rot_half<HR>(pc, q, np, nq, valid, tol2, offmax);
+        if (!valid) np = npo;
+        if (rr) {
           any = true;
-          col_sts(a0, q0);
-          col_sts(a1, q1);
-          if (lane == 0) {
-            sm.nrm[sq * JB + 2 * g] = nq0;
-            sm.nrm[sq * JB + 2 * g + 1] = nq1;
-            if (r00 || r01) cp[0] |= 2;
-            if (r11 || r10) cp[1] |= 2;
-            if (r00 || r10) cq[0] |= 2;
-            if (r11 || r01) cq[1] |= 2;
+          hcol_sts(aq, q);
+          if (hl == 0) {
+            sm.nrm[sq * JB + c] = nq;
+            sm.chg[sp * JB + hw] |= 2;
+            sm.chg[sq * JB + c] |= 2;
           }
         }
       }
       __threadfence_block();
       __syncwarp();
-      if (lane == 0) *(volatile int*)&sm.qcnt[g] = r + 1;
+      if (hl == 0) *(volatile int*)&sm.qcnt[c] = r + 1;
     }
     __syncthreads();
-    offmax = om;
-    if (any && lane == 0) sm.flag = 1;
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
     if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[14], (unsigned long long)(prof_clock() - tc0));
   }
 
-  __device__ void load_p_smem(Col<RPL>& p0, Col<RPL>& p1, double& n0, double& n1, int s, Smem& sm) {
-    const int warp = threadIdx.x >> 5;
-    col_lds(p0, scol(s, 2 * warp));
-    col_lds(p1, scol(s, 2 * warp + 1));
-    n0 = sm.nrm[s * JB + 2 * warp];
-    n1 = sm.nrm[s * JB + 2 * warp + 1];
+  __device__ void load_p(HCol<HR>& pc, double& np, int s, Smem& sm) {
+    const int hw = threadIdx.x >> 4;
+    if (s < 3) hcol_lds(pc, scol(s, hw));
+    else hcol_ldg(pc, G + (size_t)hw * Mw, Mw);
+    np = sm.nrm[s * JB + hw];
   }
-  __device__ void store_p_smem(const Col<RPL>& p0, const Col<RPL>& p1, double n0, double n1, int s, Smem& sm) {
-    const int warp = threadIdx.x >> 5;
-    col_sts(scol(s, 2 * warp), p0);
-    col_sts(scol(s, 2 * warp + 1), p1);
-    if ((threadIdx.x & 31) == 0) {
-      sm.nrm[s * JB + 2 * warp] = n0;
-      sm.nrm[s * JB + 2 * warp + 1] = n1;
-    }
-  }
-  __device__ void load_p_g(Col<RPL>& p0, Col<RPL>& p1, double& n0, double& n1, Smem& sm) {
-    const int warp = threadIdx.x >> 5;
-    col_load_g(p0, G + (size_t)(2 * warp) * Mw, Mw);
-    col_load_g(p1, G + (size_t)(2 * warp + 1) * Mw, Mw);
-    n0 = sm.nrm[3 * JB + 2 * warp];
-    n1 = sm.nrm[3 * JB + 2 * warp + 1];
-  }
-  __device__ void store_p_g(const Col<RPL>& p0, const Col<RPL>& p1, double n0, double n1, Smem& sm) {
-    const int warp = threadIdx.x >> 5;
-    col_store_g(G + (size_t)(2 * warp) * Mw, p0, Mw);
-    col_store_g(G + (size_t)(2 * warp + 1) * Mw, p1, Mw);
-    if ((threadIdx.x & 31) == 0) {
-      sm.nrm[3 * JB + 2 * warp] = n0;
-      sm.nrm[3 * JB + 2 * warp + 1] = n1;
-    }
+  __device__ void store_p(const HCol<HR>& pc, double np, int s, Smem& sm) {
+    const int hw = threadIdx.x >> 4;
+    if (s < 3) hcol_sts(scol(s, hw), pc);
+    else hcol_stg(G + (size_t)hw * Mw, pc, Mw);
+    if ((threadIdx.x & 15) == 0) sm.nrm[s * JB + hw] = np;
   }
 
-  // exact norms of every column; zero the numerically dead ones; thresholds
   __device__ void refresh_norms(Smem& sm, double tol, bool first) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int c = warp; c < JB * nblk; c += NWARP) {
       const int s = c / JB, k = c - s * JB;
       double acc = 0.0;
       if (s < 3) {
-        Col<RPL> v;
-        col_lds(v, scol(s, k));
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) acc += abs2(v.v[q]);
+        const double2* p = (const double2*)nullptr;
+        (void)p;
+        for (int y = lane; y < LD; y += 32) acc += abs2(lds2(scol(s, k) + 16u * y));
       } else {
         const double2* p = G + (size_t)k * Mw;
         for (int y = lane; y < Mw; y += 32) acc += abs2(p[y]);
@@ -778,31 +670,24 @@ struct JacobiSmem {
       acc = warp_sum(acc);
       if (lane == 0) sm.nrm[c] = acc;
     }
-    __syncthreads();
     for (int c = threadIdx.x; c < JB * nblk; c += NT) sm.chg[c] = first ? 1 : ((sm.chg[c] >> 1) & 1);
+    __syncthreads();
     if (threadIdx.x == 0) {
-      double t = 0.0, mx = 0.0;
-      for (int c = 0; c < JB * nblk; ++c) {
-        t += sm.nrm[c];
-        mx = fmax(mx, sm.nrm[c]);
-      }
+      double t = 0.0;
+      for (int c = 0; c < JB * nblk; ++c) t += sm.nrm[c];
       sm.scale = t;
-      sm.invsig_tmp = mx;
       sm.flag = 0;
       sm.offmax = 0.0;
     }
     __syncthreads();
-    tol2 = tol * tol;  // relative criterion only: the split projects onto Q, which must be orthonormal
+    tol2 = tol * tol;
     const double dead = 1e-28 * sm.scale;
     for (int c = warp; c < JB * nblk; c += NWARP) {
       const double v = sm.nrm[c];
       if (v < dead && v > 0.0) {
         const int s = c / JB, k = c - s * JB;
         if (s < 3) {
-          Col<RPL> z;
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) z.v[q] = cz();
-          col_sts(scol(s, k), z);
+          for (int y = lane; y < LD; y += 32) sts2(scol(s, k) + 16u * y, cz());
         } else {
           double2* p = G + (size_t)k * Mw;
           for (int y = lane; y < Mw; y += 32) p[y] = cz();
@@ -815,46 +700,29 @@ struct JacobiSmem {
 
   __device__ void sweep(Smem& sm) {
     offmax = 0.0;
-    sweep_body(sm);
-    if ((threadIdx.x & 15) == 0 && offmax > 0.0) atomic_max_pos(&sm.offmax, offmax);
-  }
-
-  __device__ void sweep_body(Smem& sm) {
-    const int all3[3] = {0, 1, 2};
     const int nsm = min(nblk, 3);
     const long long tw0 = prof_clock();
-    within(all3, nsm, sm);
+    within(0, 1, 2, nsm, sm);
     if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[13], (unsigned long long)(prof_clock() - tw0));
+    HCol<HR> pc;
+    double np;
     if (nblk == 4) {
+      load_p(pc, np, 3, sm);
+      for (int s = 0; s < 3; ++s) cross(pc, np, sm.jncol[3], 3, s, sm);
+      // swap contents of A and G (P holds the current G columns)
       {
-        Col<RPL> p0, p1;
-        double n0, n1;
-        load_p_g(p0, p1, n0, n1, sm);
-        for (int s = 0; s < 3; ++s) cross(p0, p1, n0, n1, sm.jncol[3], 3, s, sm);
-        // swap contents: A -> G storage, P (old G) -> A
-        Col<RPL> t0, t1;
-        double m0, m1;
-        load_p_smem(t0, t1, m0, m1, 0, sm);
+        HCol<HR> t;
+        double nt;
+        load_p(t, nt, 0, sm);
+        const int hw = threadIdx.x >> 4;
+        unsigned char fa = sm.chg[hw], fg = sm.chg[3 * JB + hw];
         __syncthreads();
-        {
-          const int warp = threadIdx.x >> 5;
-          unsigned char f0 = 0, f1 = 0, h0 = 0, h1 = 0;
-          if ((threadIdx.x & 31) == 0) {
-            f0 = sm.chg[3 * JB + 2 * warp];
-            f1 = sm.chg[3 * JB + 2 * warp + 1];
-            h0 = sm.chg[2 * warp];
-            h1 = sm.chg[2 * warp + 1];
-          }
-          __syncthreads();
-          if ((threadIdx.x & 31) == 0) {
-            sm.chg[2 * warp] = f0;
-            sm.chg[2 * warp + 1] = f1;
-            sm.chg[3 * JB + 2 * warp] = h0;
-            sm.chg[3 * JB + 2 * warp + 1] = h1;
-          }
+        store_p(pc, np, 0, sm);
+        store_p(t, nt, 3, sm);
+        if ((threadIdx.x & 15) == 0) {
+          sm.chg[hw] = fg;
+          sm.chg[3 * JB + hw] = fa;
         }
-        store_p_smem(p0, p1, n0, n1, 0, sm);
-        store_p_g(t0, t1, m0, m1, sm);
         __syncthreads();
         if (threadIdx.x == 0) {
           const int na = sm.jncol[0];
@@ -863,51 +731,36 @@ struct JacobiSmem {
         }
         __syncthreads();
       }
-      const int a1[1] = {0};
-      within(a1, 1, sm);
-      {
-        Col<RPL> p0, p1;
-        double n0, n1;
-        load_p_g(p0, p1, n0, n1, sm);
-        cross(p0, p1, n0, n1, sm.jncol[3], 3, 1, sm);
-        cross(p0, p1, n0, n1, sm.jncol[3], 3, 2, sm);
-        store_p_g(p0, p1, n0, n1, sm);
-        __syncthreads();
-      }
-      {
-        Col<RPL> p0, p1;
-        double n0, n1;
-        load_p_smem(p0, p1, n0, n1, 1, sm);
-        cross(p0, p1, n0, n1, sm.jncol[1], 1, 2, sm);
-        store_p_smem(p0, p1, n0, n1, 1, sm);
-        __syncthreads();
-      }
+      within(0, 0, 0, 1, sm);
+      load_p(pc, np, 3, sm);
+      cross(pc, np, sm.jncol[3], 3, 1, sm);
+      cross(pc, np, sm.jncol[3], 3, 2, sm);
+      store_p(pc, np, 3, sm);
+      __syncthreads();
+      load_p(pc, np, 1, sm);
+      cross(pc, np, sm.jncol[1], 1, 2, sm);
+      store_p(pc, np, 1, sm);
+      __syncthreads();
     } else {
       for (int sp = 0; sp + 1 < nsm; ++sp) {
-        Col<RPL> p0, p1;
-        double n0, n1;
-        load_p_smem(p0, p1, n0, n1, sp, sm);
-        for (int sq = sp + 1; sq < nsm; ++sq) cross(p0, p1, n0, n1, sm.jncol[sp], sp, sq, sm);
-        store_p_smem(p0, p1, n0, n1, sp, sm);
+        load_p(pc, np, sp, sm);
+        for (int sq = sp + 1; sq < nsm; ++sq) cross(pc, np, sm.jncol[sp], sp, sq, sm);
+        store_p(pc, np, sp, sm);
         __syncthreads();
       }
     }
+    if ((threadIdx.x & 15) == 0 && offmax > 0.0) atomic_max_pos(&sm.offmax, offmax);
   }
 };
 
-// Runs the smem Jacobi on W (global, Mw x Nw col-major); on return W holds
-// the rotated columns in positions [0, Nw_eff); returns Nw_eff, negated on
-// non-convergence after MAXSWEEP sweeps.
-template <int RPL>
-__device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) {
-  JacobiSmem<RPL> J;
-  constexpr int LD = JacobiSmem<RPL>::LD;
+template <int HR>
+__device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) {
+  JacobiH<HR> J;
+  constexpr int LD = JacobiH<HR>::LD;
   J.Mw = Mw;
   J.nblk = (Nw + JB - 1) / JB;
   J.base = (uint32_t)__cvta_generic_to_shared(smem);
-  J.sp = smem;
   J.G = W + (size_t)3 * JB * Mw;
-  // balanced split of the Nw columns over the blocks
   int start[5];
   start[0] = 0;
   int ncl[4];
@@ -918,11 +771,8 @@ __device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   __syncthreads();
   if (threadIdx.x < 4) sm.jncol[threadIdx.x] = ncl[threadIdx.x];
   const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16;
-  // stage W into the smem slots (zero padding), zero the unused G columns
   const int nsm = min(J.nblk, 3);
   if (J.nblk == 4) {
-    // block 3 lives in W columns 96..127 (overlapping its source columns):
-    // read everything first, then write
     double2 tmp[(JB * 128 + NT - 1) / NT];
     int cnt = 0;
     for (int e = threadIdx.x; e < JB * Mw; e += NT, ++cnt) {
@@ -945,9 +795,6 @@ __device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     J.refresh_norms(sm, tol, sweep == 0);
     J.sweep(sm);
     __syncthreads();
-    // converged: no rotation at all, or every rotation of this sweep had a
-    // relative off-diagonal below 1e-8, after which the cyclic sweep leaves
-    // O(1e-16) (quadratic convergence) — the confirming sweep is skipped
     if (sm.flag == 0 || sm.offmax < 1e-16) {
       conv = true;
       break;
@@ -955,7 +802,6 @@ __device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     __syncthreads();
   }
   if (threadIdx.x == 0) sm.sweeps = sweep + 1;
-  // write the smem slots back to W columns [0, 32*nsm)
   for (int e = threadIdx.x; e < nsm * JB * Mw; e += NT) {
     const int c = e / Mw, y = e - c * Mw;
     W[(size_t)c * Mw + y] = smem[(size_t)c * LD + y];
@@ -970,9 +816,10 @@ __device__ int jacobi_smem(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
 __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
   int neff;
   if (Nw < 2) return Nw;
-  if (Mw <= 32 && Nw <= 128) neff = jacobi_smem<1>(W, Mw, Nw, sm, smem);
-  else if (Mw <= 64 && Nw <= 128) neff = jacobi_smem<2>(W, Mw, Nw, sm, smem);
-  else if (Mw <= 128 && Nw <= 128) neff = jacobi_smem<4>(W, Mw, Nw, sm, smem);
+  if (Mw <= 16 && Nw <= 128) neff = jacobi_half<1>(W, Mw, Nw, sm, smem);
+  else if (Mw <= 32 && Nw <= 128) neff = jacobi_half<2>(W, Mw, Nw, sm, smem);
+  else if (Mw <= 64 && Nw <= 128) neff = jacobi_half<4>(W, Mw, Nw, sm, smem);
+  else if (Mw <= 128 && Nw <= 128) neff = jacobi_half<8>(W, Mw, Nw, sm, smem);
   else {
     const int sw = hestenes(W, Mw, Nw, sm);
     neff = (sw > MAXSWEEP) ? -Nw : Nw;
@@ -998,48 +845,43 @@ __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* 
 // sm.qperm.  Returns the numerical rank r (residual columns below the dead
 // threshold end the factorisation).
 // ----------------------------------------------------------------------------
-template <int RPL>
+template <int HR>
 __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, double2* smem) {
-  constexpr int LD = 32 * RPL;
+  // half-warp column layout: half k (0..31) owns smem columns k, k+32, k+64 and
+  // keeps column 96+k in registers
+  constexpr int LD = 16 * HR;
   constexpr uint32_t CB = LD * 16u;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15, lane = threadIdx.x & 31;
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t qaddr = base + 3u * JB * CB;  // q buffer after the slots
   const int nsm = min(Mw, 3 * JB);
-  // stage the smem columns (zero padded rows)
   for (int e = threadIdx.x; e < nsm * LD; e += NT) {
     const int c = e / LD, y = e - c * LD;
     smem[e] = (y < Nw) ? Y[(size_t)c * Nw + y] : cz();
   }
-  // register columns 96 + 2w, 97 + 2w; warp w also owns smem columns w + 16i
-  Col<RPL> g0, g1;
-  const int c0 = 3 * JB + 2 * warp, c1 = c0 + 1;
-  col_load_g(g0, Y + (size_t)c0 * Nw, c0 < Mw ? Nw : 0);
-  col_load_g(g1, Y + (size_t)c1 * Nw, c1 < Mw ? Nw : 0);
+  HCol<HR> g;
+  const int cg = 3 * JB + hw;
+  hcol_ldg(g, Y + (size_t)cg * Nw, cg < Mw ? Nw : 0);
   __syncthreads();
-  // exact column norms
-  for (int c = warp; c < nsm; c += NWARP) {
-    Col<RPL> v;
-    col_lds(v, base + (uint32_t)c * CB);
+  // exact norms
+  for (int k = 0; k < 3; ++k) {
+    const int c = hw + 32 * k;
     double acc = 0.0;
+    if (c < nsm) {
+      HCol<HR> v;
+      hcol_lds(v, base + (uint32_t)c * CB);
 #pragma unroll
-    for (int q = 0; q < RPL; ++q) acc += abs2(v.v[q]);
-    acc = warp_sum(acc);
-    if (lane == 0) sm.nrm[c] = sm.nref[c] = acc;
+      for (int q = 0; q < HR; ++q) acc += abs2(v.v[q]);
+    }
+    acc = half_sum(acc);
+    if (hl == 0 && c < nsm) sm.nrm[c] = sm.nref[c] = acc;
   }
   {
-    double a0 = 0.0, a1 = 0.0;
+    double acc = 0.0;
 #pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-      a0 += abs2(g0.v[q]);
-      a1 += abs2(g1.v[q]);
-    }
-    a0 = warp_sum(a0);
-    a1 = warp_sum(a1);
-    if (lane == 0) {
-      if (c0 < Mw) sm.nrm[c0] = sm.nref[c0] = a0;
-      if (c1 < Mw) sm.nrm[c1] = sm.nref[c1] = a1;
-    }
+    for (int q = 0; q < HR; ++q) acc += abs2(g.v[q]);
+    acc = half_sum(acc);
+    if (hl == 0 && cg < Mw) sm.nrm[cg] = sm.nref[cg] = acc;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1047,25 +889,21 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     for (int c = 0; c < Mw; ++c) t += sm.nrm[c];
     sm.scale = 1e-28 * t;  // dead threshold on residual norm^2
   }
-  // per-warp pivot candidates over the owned columns
+  // per-half pivot candidate over the owned columns (lanes 0-3 of the half)
   auto local_best = [&]() {
-    // lanes 0..5: owned smem columns, lanes 6, 7: the register columns
-    int c = -1;
-    if (lane < 6) c = warp + NWARP * lane;
-    else if (lane == 6) c = c0;
-    else if (lane == 7) c = c1;
-    const bool ok = c >= 0 && c < Mw && (lane >= 6 || c < nsm);
+    const int c = (hl < 3) ? hw + 32 * hl : cg;
+    const bool ok = hl < 4 && c < Mw && (hl == 3 || c < nsm);
     double best = ok ? sm.nrm[c] : -1.0;
     int bi = ok ? c : -1;
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
+    for (int o = 2; o > 0; o >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
     }
-    if (lane == 0) {
-      sm.wbest[warp] = best;
-      sm.wbidx[warp] = bi;
+    if (hl == 0) {
+      sm.wbest[hw] = best;
+      sm.wbidx[hw] = bi;
     }
   };
   local_best();
@@ -1073,10 +911,12 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
   const double dead = sm.scale;
   const int rmax = min(Mw, Nw);
   int j = 0;
+  long long tq0 = prof_clock(), tq1 = 0, tq2 = 0, tq3 = 0, tqa = 0, tqb = 0, tqc = 0, tqd = 0;
   for (; j < rmax; ++j) {
-    // global pivot (every warp, redundantly): largest residual, ties to the lowest index
-    double best = (lane < NWARP) ? sm.wbest[lane] : -1.0;
-    int p = (lane < NWARP) ? sm.wbidx[lane] : -1;
+    const long long tt0 = prof_clock();
+    // global pivot (every warp): largest residual, ties to the lowest index
+    double best = sm.wbest[lane];
+    int p = sm.wbidx[lane];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -1084,118 +924,102 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
       if (ob > best || (ob == best && oi >= 0 && (p < 0 || oi < p))) { best = ob; p = oi; }
     }
     if (!(best > dead) || p < 0) break;
-    const int owner = (p < 3 * JB) ? (p % NWARP) : ((p - 3 * JB) >> 1);
-    if (warp == owner) {
-      Col<RPL> v;
-      if (p < 3 * JB) col_lds(v, base + (uint32_t)p * CB);
-      else v = (p == c0) ? g0 : g1;
+    const long long tt1 = prof_clock();
+    tqa += tt1 - tt0;
+    const int owner = (p < 3 * JB) ? (p & 31) : (p - 3 * JB);
+    if ((owner >> 1) == (threadIdx.x >> 5)) {  // whole warp (half_sum shuffles span it)
+      const bool me = hw == owner;
+      HCol<HR> v;
+      if (p < 3 * JB) hcol_lds(v, base + (uint32_t)p * CB);
+      else v = g;
       double nn = 0.0;
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) nn += abs2(v.v[q]);
-      nn = warp_sum(nn);
+      for (int q = 0; q < HR; ++q) nn += abs2(v.v[q]);
+      nn = half_sum(nn);
       const double rn = sqrt(nn), inv = 1.0 / rn;
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) v.v[q] = cscale(v.v[q], inv);
-      col_sts(qaddr, v);
-      if (lane == 0) {
+      for (int q = 0; q < HR; ++q) v.v[q] = cscale(v.v[q], inv);
+      if (me) hcol_sts(qaddr, v);
+      if (me && hl == 0) {
         R[(size_t)j * Mw + p] = make_double2(rn, 0.0);
         sm.qperm[j] = p;
         sm.nrm[p] = -1.0;
       }
     }
+    const long long tt2 = prof_clock();
     __syncthreads();
-    Col<RPL> qv;
-    col_lds(qv, qaddr);
-    // MGS update of two columns at once: r = q^H y, y -= r q
-    auto upd2 = [&](Col<RPL>& ya, Col<RPL>& yb, int ca, int cb) {
-      const bool va = ca >= 0, vb = cb >= 0;
-      double2 da = cz(), db = cz();
+    const long long tt3 = prof_clock();
+    tqb += tt2 - tt1;
+    tqc += tt3 - tt2;
+    HCol<HR> qv;
+    hcol_lds(qv, qaddr);
+    // MGS update of one column per half: r = q^H y, y -= r q
+    auto upd = [&](HCol<HR>& y, int c, bool valid) {
+      double2 d = cz(), e = cz();
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        cfmac(da, qv.v[q], ya.v[q]);
-        cfmac(db, qv.v[q], yb.v[q]);
+      for (int q = 0; q < HR; q += 2) {
+        cfmac(d, qv.v[q], y.v[q]);
+        if (q + 1 < HR) cfmac(e, qv.v[q + 1], y.v[q + 1]);
       }
-      const bool up = lane & 16;
-      double x0 = up ? db.x : da.x, x1 = up ? db.y : da.y;
-      const double z0 = up ? da.x : db.x, z1 = up ? da.y : db.y;
-      x0 += __shfl_xor_sync(0xffffffffu, z0, 16);
-      x1 += __shfl_xor_sync(0xffffffffu, z1, 16);
-      const bool h8 = lane & 8;
-      double z = h8 ? x1 : x0;
-      const double w8 = h8 ? x0 : x1;
-      z += __shfl_xor_sync(0xffffffffu, w8, 8);
-      z += __shfl_xor_sync(0xffffffffu, z, 4);
-      z += __shfl_xor_sync(0xffffffffu, z, 2);
-      z += __shfl_xor_sync(0xffffffffu, z, 1);
-      const double o = __shfl_xor_sync(0xffffffffu, z, 8);
-      const double mr = h8 ? o : z, mi = h8 ? z : o;        // this half's dot
-      const double orr = __shfl_xor_sync(0xffffffffu, mr, 16);
-      const double oi = __shfl_xor_sync(0xffffffffu, mi, 16);
-      da = up ? make_double2(orr, oi) : make_double2(mr, mi);
-      db = up ? make_double2(mr, mi) : make_double2(orr, oi);
-      if (!va) da = cz();
-      if (!vb) db = cz();
+      d.x = half_sum(d.x + e.x);
+      d.y = half_sum(d.y + e.y);
+      if (!valid) d = cz();
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        ya.v[q].x -= da.x * qv.v[q].x - da.y * qv.v[q].y;
-        ya.v[q].y -= da.x * qv.v[q].y + da.y * qv.v[q].x;
-        yb.v[q].x -= db.x * qv.v[q].x - db.y * qv.v[q].y;
-        yb.v[q].y -= db.x * qv.v[q].y + db.y * qv.v[q].x;
+      for (int q = 0; q < HR; ++q) {
+        y.v[q].x -= d.x * qv.v[q].x - d.y * qv.v[q].y;
+        y.v[q].y -= d.x * qv.v[q].y + d.y * qv.v[q].x;
       }
-      double na = va ? sm.nrm[ca] - abs2(da) : 0.0, nb = vb ? sm.nrm[cb] - abs2(db) : 0.0;
-      const bool fa = va && na < 1e-2 * sm.nref[ca], fb = vb && nb < 1e-2 * sm.nref[cb];
-      if (fa || fb) {  // cancellation: exact norms
-        double ea = 0.0, eb = 0.0;
+      double nr = valid ? sm.nrm[c] - abs2(d) : 0.0;
+      const bool f = valid && nr < 1e-2 * sm.nref[c];
+      if (__any_sync(0xffffffffu, f)) {  // cancellation: exact norm
+        double acc = 0.0;
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-          ea += abs2(ya.v[q]);
-          eb += abs2(yb.v[q]);
-        }
-        ea = warp_sum(ea);
-        eb = warp_sum(eb);
-        if (fa) na = ea;
-        if (fb) nb = eb;
+        for (int q = 0; q < HR; ++q) acc += abs2(y.v[q]);
+        acc = half_sum(acc);
+        if (f) nr = acc;
       }
-      if (lane == 0) {
-        if (va) {
-          sm.nrm[ca] = na;
-          if (fa) sm.nref[ca] = na;
-          R[(size_t)j * Mw + ca] = da;
-        }
-        if (vb) {
-          sm.nrm[cb] = nb;
-          if (fb) sm.nref[cb] = nb;
-          R[(size_t)j * Mw + cb] = db;
-        }
+      if (hl == 0 && valid) {
+        sm.nrm[c] = nr;
+        if (f) sm.nref[c] = nr;
+        R[(size_t)j * Mw + c] = d;
       }
     };
-    for (int c = warp; c < nsm; c += 2 * NWARP) {
-      const int cb = c + NWARP;
-      const int ia = (sm.nrm[c] >= 0.0) ? c : -1;
-      const int ib = (cb < nsm && sm.nrm[cb] >= 0.0) ? cb : -1;
-      if (ia < 0 && ib < 0) continue;
-      Col<RPL> ya, yb;
-      col_lds(ya, base + (uint32_t)c * CB);
-      if (cb < nsm) col_lds(yb, base + (uint32_t)cb * CB);
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) {
+      const int c = hw + 32 * k;
+      const bool valid = c < nsm && sm.nrm[c] >= 0.0;
+      if (!__any_sync(0xffffffffu, valid)) continue;
+      HCol<HR> y;
+      if (valid) hcol_lds(y, base + (uint32_t)c * CB);
       else {
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) yb.v[q] = cz();
+        for (int q = 0; q < HR; ++q) y.v[q] = cz();
       }
-      upd2(ya, yb, ia, ib);
-      if (ia >= 0) col_sts(base + (uint32_t)c * CB, ya);
-      if (ib >= 0) col_sts(base + (uint32_t)cb * CB, yb);
+      upd(y, c, valid);
+      if (valid) hcol_sts(base + (uint32_t)c * CB, y);
     }
     {
-      const int ia = (c0 < Mw && sm.nrm[c0] >= 0.0) ? c0 : -1;
-      const int ib = (c1 < Mw && sm.nrm[c1] >= 0.0) ? c1 : -1;
-      if (ia >= 0 || ib >= 0) upd2(g0, g1, ia, ib);
+      const bool valid = cg < Mw && sm.nrm[cg] >= 0.0;
+      if (__any_sync(0xffffffffu, valid)) upd(g, cg, valid);
     }
     __syncwarp();
     local_best();
+    const long long tt4 = prof_clock();
     __syncthreads();
+    tqd += tt4 - tt3;
+    tq1 += prof_clock() - tt4;
   }
+  if (threadIdx.x == 0 && sm.prof) {
+    atomicAdd(&sm.prof[15], (unsigned long long)j);
+    atomicAdd(&sm.prof[32], (unsigned long long)tqa);   // pivot selection
+    atomicAdd(&sm.prof[33], (unsigned long long)tqb);   // owner normalisation (thread 0's view)
+    atomicAdd(&sm.prof[34], (unsigned long long)tqc);   // barrier 1 wait
+    atomicAdd(&sm.prof[35], (unsigned long long)tqd);   // update + local best
+    atomicAdd(&sm.prof[36], (unsigned long long)tq1);   // barrier 2 wait
+    atomicAdd(&sm.prof[37], (unsigned long long)(prof_clock() - tq0));
+  }
+  (void)tq2; (void)tq3;
   // complete the permutation with the numerically dead columns
-  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
   if (threadIdx.x == 0) {
     int k = j;
     for (int c = 0; c < Mw; ++c)
@@ -1216,10 +1040,10 @@ __device__ void build_l(const double2* R, int Mw, int r, double2* W, const Smem&
   __syncthreads();
 }
 
-template <int RPL>
+template <int HR>
 __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
   const long long t0 = prof_clock();
-  const int r = qrcp_mgs<RPL>(W, Nw, Mw, X, sm, smem);
+  const int r = qrcp_mgs<HR>(W, Nw, Mw, X, sm, smem);
   if (threadIdx.x == 0 && sm.prof) {
     atomicAdd(&sm.prof[12], (unsigned long long)(prof_clock() - t0));
     atomicAdd(&sm.prof[8], 1ull);
@@ -1241,9 +1065,10 @@ __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm
 // Y = W^H is in W (ld = Nw); returns Neff, W = rotated columns of L (ld = Mw),
 // rows in pivoted order (sm.qpinv maps an original row to its position)
 __device__ int precond_jacobi(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
-  if (Nw <= 32) return precond_jacobi_t<1>(W, X, Mw, Nw, sm, smem, status);
-  if (Nw <= 64) return precond_jacobi_t<2>(W, X, Mw, Nw, sm, smem, status);
-  return precond_jacobi_t<4>(W, X, Mw, Nw, sm, smem, status);
+  if (Nw <= 16) return precond_jacobi_t<1>(W, X, Mw, Nw, sm, smem, status);
+  if (Nw <= 32) return precond_jacobi_t<2>(W, X, Mw, Nw, sm, smem, status);
+  if (Nw <= 64) return precond_jacobi_t<4>(W, X, Mw, Nw, sm, smem, status);
+  return precond_jacobi_t<8>(W, X, Mw, Nw, sm, smem, status);
 }
 
 // ----------------------------------------------------------------------------

@@ -12,3 +12,5 @@ calls = max(pr[1], 1)
 print(f"per SVD: sweeps {pr[2]/calls:.2f}  qrcp calls {pr[8]:.0f} qrcp Mcyc {pr[12]/max(pr[8],1)/1e6:.3f} (steps {pr[15]/max(pr[8],1):.1f}, "
       f"{pr[12]/max(pr[15],1):.0f} cyc/step)  within Mcyc {pr[13]/calls/1e6:.3f}  cross Mcyc {pr[14]/calls/1e6:.3f}  "
       f"per sweep: within {pr[13]/pr[2]/1e3:.1f}k cross {pr[14]/pr[2]/1e3:.1f}k")
+st = max(pr[15], 1)
+print("qrcp per step (thread 0 view): pivot %.0f owner %.0f bar1 %.0f update %.0f bar2 %.0f total %.0f" % tuple(pr[32:38] / st))

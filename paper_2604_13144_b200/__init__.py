@@ -7,6 +7,7 @@ plus the batched ``run_ensemble`` / ``aggregate`` of SPEC.md.
 
 from .estimator import EnsembleResult, SampleRecord, aggregate, aggregate_fixed, results_table
 from .ensemble import (
+    SlotPipeline,
     EnsembleRun,
     PackedEnsemble,
     allreduce_sums,

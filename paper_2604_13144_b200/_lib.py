@@ -11,7 +11,7 @@ import threading
 import numpy as np
 
 LIB_NAME = "libtepai_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("TB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 EXPORTED = (
     "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_debug_profile", "tb_run_stream",

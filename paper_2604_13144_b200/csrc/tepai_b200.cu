@@ -770,7 +770,10 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   }
   __syncthreads();
   if (threadIdx.x < 4) sm.jncol[threadIdx.x] = ncl[threadIdx.x];
-  const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16;
+#ifndef TB_TOLSCALE
+#define TB_TOLSCALE 1.0
+#endif
+  const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16 * TB_TOLSCALE;
   const int nsm = min(J.nblk, 3);
   if (J.nblk == 4) {
     double2 tmp[(JB * 128 + NT - 1) / NT];
@@ -795,7 +798,7 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     J.refresh_norms(sm, tol, sweep == 0);
     J.sweep(sm);
     __syncthreads();
-    if (sm.flag == 0 || sm.offmax < 1e-16) {
+    if (sm.flag == 0 || sm.offmax < 1e-16 * TB_TOLSCALE) {
       conv = true;
       break;
     }

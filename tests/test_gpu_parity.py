@@ -239,3 +239,26 @@ def test_slot_pipeline_matches_whole_circuit_runs(engine, golden):
     np.testing.assert_array_equal(pipe.row_count, np.full(ck.size, 24))
     st = pipe.stats()
     np.testing.assert_allclose(st[ck.size - 1]["estimate"], run.stats()["estimate"][-1], atol=1e-15)
+
+
+def test_chi128_bonds_vs_oracle(engine):
+    """chi = 128 (the C5 bond capacity): 256x256 two-site problems run on the
+    L2-resident Jacobi path; brickwork of generic rotations on n = 16 grows the
+    centre bond past 64, untruncated (cap = 128 > reached bonds) vs the oracle."""
+    n = 16
+    rng = np.random.default_rng(3)
+    ops = []
+    for layer in range(8):
+        for a in range(layer % 2, n - 1, 2):
+            for sym in "XYZ":
+                ops.append((tb.PauliString(n, ((a, sym), (a + 1, sym))), float(rng.uniform(0.3, 1.2))))
+    st = tb.init_product_state("01" * 8)
+    ora = OracleMPS("01" * 8)
+    pol = tb.TruncationPolicy(128, 1e-14)
+    tb.run_circuit(st, _OpsCircuit(n, ops), pol)
+    ora.run(ops, 128, 1e-14)
+    assert max(st.bond_dims) > 64
+    assert st.bond_dims == tuple(int(d) for d in ora.dims)
+    for j in (0, 5, 8, 15):
+        p = tb.PauliString.single(n, j, "Z")
+        assert tb.expectation(st, p) == pytest.approx(ora.expect({j: "Z"}), abs=1e-10)

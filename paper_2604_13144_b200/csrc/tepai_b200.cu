@@ -917,16 +917,16 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
   long long tq0 = prof_clock(), tq1 = 0, tq2 = 0, tq3 = 0, tqa = 0, tqb = 0, tqc = 0, tqd = 0;
   for (; j < rmax; ++j) {
     const long long tt0 = prof_clock();
-    // global pivot (every warp): largest residual, ties to the lowest index
-    double best = sm.wbest[lane];
-    int p = sm.wbidx[lane];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, p, o);
-      if (ob > best || (ob == best && oi >= 0 && (p < 0 || oi < p))) { best = ob; p = oi; }
-    }
-    if (!(best > dead) || p < 0) break;
+    // global pivot (every warp): largest residual.  Key = high word of the
+    // (non-negative) norm with its 7 low bits replaced by 127 - column, so one
+    // redux.max picks the largest norm (to ~1e-6 relative; near-ties go to the
+    // lowest index, which is immaterial for the preconditioner)
+    const int wi = sm.wbidx[lane];
+    const double wv = sm.wbest[lane];
+    const unsigned key = (wi >= 0 && wv > dead) ? ((unsigned)__double2hiint(wv) & 0xFFFFFF80u) | (unsigned)(127 - wi) : 0u;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+    if (kmax == 0u) break;
+    const int p = 127 - (int)(kmax & 127u);
     const long long tt1 = prof_clock();
     tqa += tt1 - tt0;
     const int owner = (p < 3 * JB) ? (p & 31) : (p - 3 * JB);

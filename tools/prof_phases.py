@@ -6,7 +6,9 @@ exec(open("tools/prof_svd.py").read().split("lib, ctx")[0])  # build matrices a 
 lib, ctx = _lib.load(), _lib.context(0)
 s = np.zeros((b, min(m, n)))
 for rep in range(2):
-    _lib.check(lib.tb_svd(ctx, a.ctypes.data, b, m, n, s.ctypes.data, None, None), ctx)
+    rc = lib.tb_svd(ctx, a.ctypes.data, b, m, n, s.ctypes.data, None, None)
+    if rc:
+        print("tb_svd rc", rc, "(diagnostic run continues)")
 pr = _lib.debug_profile().astype(np.float64)
 calls = max(pr[1], 1)
 print(f"per SVD: sweeps {pr[2]/calls:.2f}  qrcp calls {pr[8]:.0f} qrcp Mcyc {pr[12]/max(pr[8],1)/1e6:.3f} (steps {pr[15]/max(pr[8],1):.1f}, "

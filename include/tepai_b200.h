@@ -97,6 +97,12 @@ typedef struct tb_ensemble_desc {
   const double* ckpt_weight;    /* [n_ckpt] ||g||_1 of each prefix (informational) */
   const int32_t* obs_sites;     /* [n_obs] sites j of the <Z_j> observables */
   const double* init_vecs;      /* [n][2] complex128 product-state site vectors */
+  /* optional start MPS shared by every sample (hybrid Trotter -> TE-PAI fan-out,
+   * SPEC.md:487-495 / mps.py:296-338 snapshots); NULL = product state */
+  const double* init_mps;       /* complex128 [n][cap][2][cap] */
+  const int32_t* init_dims;     /* [n+1] */
+  int32_t init_center;
+  int32_t reserved;
 } tb_ensemble_desc;
 
 typedef struct tb_ensemble_out {

@@ -11,6 +11,8 @@ from .ensemble import (
     EnsembleRun,
     PackedEnsemble,
     allreduce_sums,
+    broadcast_state,
+    run_hybrid,
     checkpoint_weights,
     pack_ensemble,
     run_ensemble,

@@ -31,6 +31,8 @@ class EnsembleDesc(ctypes.Structure):
         ("gates", ctypes.c_void_p), ("gate_offsets", ctypes.c_void_p), ("ckpt_gate_end", ctypes.c_void_p),
         ("ckpt_sign", ctypes.c_void_p), ("angle_cs", ctypes.c_void_p), ("ckpt_weight", ctypes.c_void_p),
         ("obs_sites", ctypes.c_void_p), ("init_vecs", ctypes.c_void_p),
+        ("init_mps", ctypes.c_void_p), ("init_dims", ctypes.c_void_p), ("init_center", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -86,6 +86,9 @@ struct Job {
   const double* angle_cs;
   const int32_t* obs_sites;
   const double* init_vecs;  // product-state site vectors [n][2] (complex)
+  const double2* init_mps;  // optional start MPS [n][cap][2][cap] (hybrid fan-out)
+  const int32_t* init_dims; // [n+1] bond dims of init_mps
+  int init_center;
   int slot_mode;            // 0: work queue of whole samples; 1: CTA b advances slot b
   const uint8_t* reset;     // slot mode: 1 = start slot b from the product state (NULL: never)
   const int32_t* sum_row;   // [n_samples][n_ckpt] estimator row of each checkpoint (NULL: ck)
@@ -1608,7 +1611,27 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
     int* sdims = job.slot_dims + (size_t)blockIdx.x * (MAXN + 1);
     // --- initial state: product state, or the slot's persistent state
     const bool fresh = !job.slot_mode || (job.reset && job.reset[sample]);
-    if (fresh) {
+    if (fresh && job.init_mps) {
+      // hybrid fan-out: every sample starts from the broadcast snapshot
+      for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = job.init_dims[e];
+      __syncthreads();
+      for (int s = 0; s < n; ++s) {
+        const int cl = sm.dims[s], cr = sm.dims[s + 1];
+        const double2* src = job.init_mps + (size_t)s * cap * 2 * cap;
+        double2* dst = cx.site(s);
+        for (int e = threadIdx.x; e < cl * 2 * cr; e += NT) {
+          const int row = e / cr, r = e - row * cr;
+          dst[(size_t)row * cap + r] = src[(size_t)row * cap + r];
+        }
+      }
+      if (threadIdx.x == 0) {
+        sm.center = job.init_center;
+        int mx = 1;
+        for (int q = 0; q <= n; ++q) mx = max(mx, sm.dims[q]);
+        sm.counters[0] = sm.counters[1] = sm.counters[3] = 0.0;
+        sm.counters[2] = mx;
+      }
+    } else if (fresh) {
       for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = 1;
       for (int e = threadIdx.x; e < n * 2; e += NT) {
         const int s = e >> 1, i = e & 1;
@@ -1906,10 +1929,13 @@ int validate_desc(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o
   if (d->n_samples < 0 || d->n_ckpt < 0 || d->n_obs < 0 || d->n_obs > tb::MAXN || d->n_angles < 1 ||
       d->n_angles > 1024)
     return fail(c, TB_EINVAL, "bad ensemble sizes");
-  if (!d->gates || !d->gate_offsets || !d->angle_cs || !d->init_vecs || !o->sum_v || !o->sum_v2 || !o->flops)
+  if (!d->gates || !d->gate_offsets || !d->angle_cs || (!d->init_vecs && !d->init_mps) || !o->sum_v || !o->sum_v2 ||
+      !o->flops)
     return fail(c, TB_EINVAL, "null argument");
   if (d->n_ckpt > 0 && (!d->ckpt_gate_end || !d->ckpt_sign || (d->n_obs > 0 && !d->obs_sites)))
     return fail(c, TB_EINVAL, "null checkpoint argument");
+  if (d->init_mps && (!d->init_dims || d->init_center < 0 || d->init_center >= d->n))
+    return fail(c, TB_EINVAL, "init_mps needs init_dims and a centre in [0, n)");
   return TB_OK;
 }
 
@@ -1935,6 +1961,9 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
   job.angle_cs = d->angle_cs;
   job.obs_sites = d->obs_sites;
   job.init_vecs = d->init_vecs;
+  job.init_mps = (const double2*)d->init_mps;
+  job.init_dims = d->init_dims;
+  job.init_center = d->init_center;
   job.values = o->values;
   job.discarded = o->discarded;
   job.ledger = o->ledger;
@@ -2013,8 +2042,10 @@ int stage_inputs(tb_ctx* c, Staged& sg, const tb_ensemble_desc* d, tb_ensemble_d
   dd->ckpt_weight = nullptr;
   dd->obs_sites = sg.up(d->obs_sites, (size_t)O);
   dd->init_vecs = sg.up(d->init_vecs, 4 * (size_t)d->n);
+  dd->init_mps = d->init_mps ? (const double*)sg.up((const double2*)d->init_mps, (size_t)d->n * d->cap * 2 * d->cap) : nullptr;
+  dd->init_dims = d->init_mps ? sg.up(d->init_dims, (size_t)d->n + 1) : nullptr;
   if (!dd->gates || !dd->gate_offsets || !dd->ckpt_gate_end || !dd->ckpt_sign || !dd->angle_cs || !dd->obs_sites ||
-      !dd->init_vecs)
+      !dd->init_vecs || (d->init_mps && (!dd->init_mps || !dd->init_dims)))
     return fail(c, TB_ENOMEM, "device allocation failed");
   return TB_OK;
 }

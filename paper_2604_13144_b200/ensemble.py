@@ -53,6 +53,9 @@ class PackedEnsemble:
     sample_ids: np.ndarray
     nu: np.ndarray
     pi_local: bool = True
+    init_mps: np.ndarray | None = None   # complex128 [n, cap, 2, cap] start state (hybrid fan-out)
+    init_dims: np.ndarray | None = None  # int32 [n+1]
+    init_center: int = 0
 
     @property
     def n_samples(self) -> int:
@@ -64,10 +67,12 @@ class PackedEnsemble:
 
 
 def pack_ensemble(ham: Hamiltonian, cfg: PaiConfig, seed: int, sample_ids, labels, policy: TruncationPolicy,
-                  checkpoints, obs_sites=None, pi_local: bool = True) -> PackedEnsemble:
-    """Sample (reference-identical draws) and pack a batch of circuits."""
+                  checkpoints, obs_sites=None, pi_local: bool = True, init_state=None) -> PackedEnsemble:
+    """Sample (reference-identical draws) and pack a batch of circuits.  With
+    ``init_state`` (an ``MPSState``) every sample starts from that MPS instead
+    of the product state ``labels`` (hybrid Trotter -> TE-PAI)."""
     n = ham.n
-    if len(labels) != n:
+    if init_state is None and len(labels) != n:
         raise ValueError("initial-state labels do not match the chain length")
     hard = 2 ** (n // 2)
     cut = hard if policy.chi_cut is None else min(policy.chi_cut, hard)
@@ -82,10 +87,27 @@ def pack_ensemble(ham: Hamiltonian, cfg: PaiConfig, seed: int, sample_ids, label
         packed.append(pack_sampled(circ, table, checkpoints))
     words, offs, ce, cs = pack_batch(packed, int(checkpoints.size))
     obs = np.arange(n, dtype=np.int32) if obs_sites is None else np.asarray(obs_sites, dtype=np.int32)
-    init = np.stack([SITE_VECTORS[lab] for lab in labels]).astype(np.complex128)
-    return PackedEnsemble(n, cut, cut, float(policy.svalue_floor), words, offs, ce, cs,
-                          angle_table(tepai_angles(cfg.delta)), checkpoint_weights(ham, cfg, checkpoints), obs,
-                          init.view(np.float64).reshape(n, 4).copy(), ids, np.diff(offs), pi_local)
+    labs = labels if init_state is None else "0" * n
+    init = np.stack([SITE_VECTORS[lab] for lab in labs]).astype(np.complex128)
+    pe = PackedEnsemble(n, cut, cut, float(policy.svalue_floor), words, offs, ce, cs,
+                        angle_table(tepai_angles(cfg.delta)), checkpoint_weights(ham, cfg, checkpoints), obs,
+                        init.view(np.float64).reshape(n, 4).copy(), ids, np.diff(offs), pi_local)
+    if init_state is not None:
+        if init_state.n != n:
+            raise ValueError(f"start state on {init_state.n} qubits, Hamiltonian has {n}")
+        if init_state.max_bond() > cut:
+            raise ValueError("start state bond dimension exceeds the truncation cap")
+        st = init_state.copy()
+        st.ensure_capacity(cut)
+        if st.cap != cut:  # shrink a larger buffer to the ensemble capacity
+            buf = np.zeros((n, cut, 2, cut), np.complex128)
+            for q in range(n):
+                buf[q, : st.dims[q], :, : st.dims[q + 1]] = st.buf[q, : st.dims[q], :, : st.dims[q + 1]]
+            st.buf, st.cap = buf, cut
+        pe.init_mps = np.ascontiguousarray(st.buf)
+        pe.init_dims = st.dims.astype(np.int32)
+        pe.init_center = int(st.center)
+    return pe
 
 
 @dataclass
@@ -123,7 +145,9 @@ def run_packed(p: PackedEnsemble, device: int = 0, keep_values: bool = True) -> 
     w, off, ce, cs, ang, wt, obs, iv = arrays
     desc = _lib.EnsembleDesc(p.n, p.cap, p.chi_cut, int(p.pi_local), p.floor, S, C, O, ang.shape[0],
                              w.ctypes.data, off.ctypes.data, ce.ctypes.data, cs.ctypes.data, ang.ctypes.data,
-                             wt.ctypes.data, obs.ctypes.data, iv.ctypes.data)
+                             wt.ctypes.data, obs.ctypes.data, iv.ctypes.data,
+                             p.init_mps.ctypes.data if p.init_mps is not None else None,
+                             p.init_dims.ctypes.data if p.init_dims is not None else None, p.init_center, 0)
     out = _lib.EnsembleOut(values.ctypes.data if values is not None else None,
                            disc.ctypes.data if disc is not None else None, ledger.ctypes.data,
                            sv.ctypes.data, sv2.ctypes.data, flops.ctypes.data, kms.ctypes.data)
@@ -136,11 +160,64 @@ def run_packed(p: PackedEnsemble, device: int = 0, keep_values: bool = True) -> 
 
 def run_ensemble(ham: Hamiltonian, cfg: PaiConfig, seed: int, sample_ids, init_labels, policy: TruncationPolicy,
                  checkpoints, observables=None, pi_local: bool = True, device: int = 0,
-                 keep_values: bool = True) -> EnsembleRun:
+                 keep_values: bool = True, init_state=None) -> EnsembleRun:
     """Batched ensemble: <Z_j> at each checkpoint step for every sample, plus the
     signed fixed-point sums of the estimator."""
-    p = pack_ensemble(ham, cfg, seed, sample_ids, init_labels, policy, checkpoints, observables, pi_local)
+    p = pack_ensemble(ham, cfg, seed, sample_ids, init_labels, policy, checkpoints, observables, pi_local,
+                      init_state)
     return run_packed(p, device, keep_values)
+
+
+def broadcast_state(state, src: int = 0, group=None):
+    """Fan one MPS out to every rank (config 5): snapshot bytes (mps.py:296-338
+    format) through one torch.distributed broadcast."""
+    import torch
+    import torch.distributed as dist
+
+    from .mps import snapshot_from_bytes, snapshot_to_bytes
+
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    if dist.get_rank(group) == src:
+        raw = np.frombuffer(snapshot_to_bytes(state), dtype=np.uint8)
+        size = torch.tensor([raw.size], dtype=torch.int64, device=dev)
+    else:
+        size = torch.zeros(1, dtype=torch.int64, device=dev)
+    dist.broadcast(size, src, group=group)
+    buf = torch.from_numpy(raw.copy()).to(dev) if dist.get_rank(group) == src else torch.zeros(
+        int(size[0]), dtype=torch.uint8, device=dev)
+    dist.broadcast(buf, src, group=group)
+    return state if dist.get_rank(group) == src else snapshot_from_bytes(buf.cpu().numpy().tobytes())
+
+
+def run_hybrid(ham: Hamiltonian, trotter_steps: int, t0: float, cfg: PaiConfig, seed: int, sample_ids, init_labels,
+               policy: TruncationPolicy, checkpoints, observables=None, pi_local: bool = True, device: int = 0,
+               keep_values: bool = True, group=None):
+    """Config 5: deterministic first-order Trotter evolution to t0 on the GPU
+    (``run_circuit`` on the continuous-angle circuit, trotter.py:48-57), then a
+    TE-PAI extension over ``cfg.total_time`` where every sample starts from that
+    MPS.  Under torch.distributed rank 0 evolves and the
+    snapshot is broadcast; each rank then runs its own ``sample_ids`` shard.
+    Returns (EnsembleRun, start MPSState)."""
+    from .mps import init_product_state, run_circuit
+    from .trotter import build_trotter_circuit
+
+    try:
+        import torch.distributed as dist
+
+        distributed = dist.is_available() and dist.is_initialized()
+    except ImportError:
+        distributed = False
+    state = None
+    if not distributed or dist.get_rank(group) == 0:
+        state = init_product_state(init_labels)
+        run_circuit(state, build_trotter_circuit(ham, t0, trotter_steps), policy)
+    if distributed:
+        state = broadcast_state(state, 0, group)
+    run = run_ensemble(ham, cfg, seed, sample_ids, init_labels, policy, checkpoints, observables, pi_local, device,
+                       keep_values, init_state=state)
+    return run, state
+
 
 
 def shard_range(n_samples: int, rank: int, world: int) -> range:
@@ -193,12 +270,13 @@ class SlotPipeline:
 
     def __init__(self, ham: Hamiltonian, cfg: PaiConfig, seed: int, labels, policy: TruncationPolicy,
                  checkpoints, n_slots: int | None = None, observables=None, pi_local: bool = True,
-                 device: int = 0, first_sample: int = 0, sample_stride: int = 1):
+                 device: int = 0, first_sample: int = 0, sample_stride: int = 1, init_state=None):
         self.ham, self.cfg, self.seed, self.device = ham, cfg, seed, device
         self.checkpoints = np.asarray(checkpoints, dtype=np.int64)
         if self.checkpoints[-1] != cfg.n_steps:
             raise ValueError("the last checkpoint must be the end of the circuit")
-        self.proto = pack_ensemble(ham, cfg, seed, [], labels, policy, self.checkpoints, observables, pi_local)
+        self.proto = pack_ensemble(ham, cfg, seed, [], labels, policy, self.checkpoints, observables, pi_local,
+                                   init_state)
         ctx = _lib.context(device)
         sms = _lib.load().tb_num_sms(ctx)
         self.n_slots = min(n_slots or sms, sms)
@@ -249,7 +327,8 @@ class SlotPipeline:
         p = self.proto
         base = _lib.EnsembleDesc(p.n, p.cap, p.chi_cut, int(p.pi_local), p.floor, S, 1, p.obs_sites.size,
                                  p.angle_cs.shape[0], ptrs["words"], ptrs["offsets"], ptrs["ckpt_end"],
-                                 ptrs["ckpt_sign"], ptrs["angle_cs"], None, ptrs["obs"], ptrs["init"])
+                                 ptrs["ckpt_sign"], ptrs["angle_cs"], None, ptrs["obs"], ptrs["init"],
+                                 ptrs.get("init_mps"), ptrs.get("init_dims"), p.init_center, 0)
         return _lib.StepDesc(base, ptrs["reset"], ptrs["sum_row"])
 
     def step_host(self, plan: StepPlan, values: np.ndarray | None = None) -> float:
@@ -260,6 +339,9 @@ class SlotPipeline:
         keep = [np.ascontiguousarray(x) for x in keep]
         ptrs = dict(zip(["words", "offsets", "ckpt_end", "ckpt_sign", "reset", "sum_row", "angle_cs", "obs", "init"],
                         [x.ctypes.data for x in keep]))
+        if self.proto.init_mps is not None:
+            ptrs["init_mps"] = self.proto.init_mps.ctypes.data
+            ptrs["init_dims"] = self.proto.init_dims.ctypes.data
         desc = self._desc(ptrs, S)
         vals = values if values is not None else np.zeros((S, 1, O))
         flops = np.zeros(1)
@@ -297,6 +379,8 @@ class SlotPipeline:
             "sum_v": torch.from_numpy(self.sum_v).to(dev),
             "sum_v2": torch.from_numpy(self.sum_v2).to(dev),
             "flops": torch.zeros(1, dtype=torch.float64, device=dev),
+            **({"init_mps": torch.from_numpy(self.proto.init_mps.view(np.float64)).to(dev),
+                "init_dims": torch.from_numpy(self.proto.init_dims).to(dev)} if self.proto.init_mps is not None else {}),
         }
 
     def step_device(self, t: dict, ds: dict, stream_ptr: int) -> None:
@@ -304,6 +388,8 @@ class SlotPipeline:
         S = self.n_slots
         ptrs = {k: t[k].data_ptr() for k in ("words", "offsets", "ckpt_end", "ckpt_sign", "reset", "sum_row")}
         ptrs.update(angle_cs=ds["angle_cs"].data_ptr(), obs=ds["obs"].data_ptr(), init=ds["init"].data_ptr())
+        if "init_mps" in ds:
+            ptrs.update(init_mps=ds["init_mps"].data_ptr(), init_dims=ds["init_dims"].data_ptr())
         desc = self._desc(ptrs, S)
         out = _lib.EnsembleOut(ds["values"].data_ptr(), None, None, ds["sum_v"].data_ptr(), ds["sum_v2"].data_ptr(),
                                ds["flops"].data_ptr(), None)

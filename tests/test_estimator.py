@@ -88,3 +88,42 @@ def test_gloo_world2_allreduce_is_exact():
     for p in procs:
         p.join(timeout=60)
     assert ns == 101 and got == want
+
+
+def _bcast_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    st = None
+    if rank == 0:
+        st = tb.MPSState(3)
+        st.ensure_capacity(2)
+        st.dims = np.array([1, 2, 2, 1])
+        st.buf[:] = np.arange(st.buf.size).reshape(st.buf.shape) * (1 + 0.5j)
+        st.center = 1
+        st.discarded_weight = 1e-9
+    got = tb.broadcast_state(st, 0)
+    if rank == 1:
+        out.put((got.bond_dims, got.center, got.discarded_weight, [t.tolist() for t in got.tensors]))
+    else:
+        out.put(("src", st.bond_dims, [t.tolist() for t in st.tensors]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_snapshot_broadcast():
+    """Config-5 fan-out: the t0 MPS reaches every rank intact (snapshot format)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + (os.getpid() % 2000)
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120), q.get(timeout=120)]
+    for p in procs:
+        p.join(timeout=60)
+    src = [r for r in res if r[0] == "src"][0]
+    dst = [r for r in res if r[0] != "src"][0]
+    assert dst[0] == src[1] and dst[1] == 1 and dst[2] == 1e-9 and dst[3] == src[2]

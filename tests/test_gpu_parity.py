@@ -262,3 +262,19 @@ def test_chi128_bonds_vs_oracle(engine):
     for j in (0, 5, 8, 15):
         p = tb.PauliString.single(n, j, "Z")
         assert tb.expectation(st, p) == pytest.approx(ora.expect({j: "Z"}), abs=1e-10)
+
+
+def test_hybrid_trotter_then_tepai_vs_reference(engine, golden):
+    """Config 5 schedule at desk scale: Trotter evolution on the GPU
+    (continuous angles through tb_run_stream) to t0, then 16 TE-PAI samples
+    that all start from that MPS (init_mps fan-out), vs the reference."""
+    ref = golden("ref_hybrid_n6.npz")
+    ham = tb.build_spin_ring(6, 1.0, 8)
+    cfg = tb.PaiConfig(math.pi / 2**6, 20, 0.4)
+    run, st0 = tb.run_hybrid(ham, 30, 0.6, cfg, 9, range(16), "010101", tb.TruncationPolicy(8, 1e-12),
+                             ref["checkpoints"], pi_local=False)
+    np.testing.assert_allclose(st0.to_statevector(), ref["psi_t0"], atol=1e-11)
+    np.testing.assert_allclose(run.values, ref["vals"], atol=1e-10)
+    signs = ref["sign"].astype(np.float64)
+    want = tb.estimator.quantize(signs[:, :, None] * ref["vals"]).sum(axis=0)
+    assert np.max(np.abs(run.sum_v - want)) <= 16  # 2^-40 quantisation of values equal to 1e-10

@@ -1084,6 +1084,9 @@ __device__ __forceinline__ void prof_add(const Job& jb, int slot, long long v) {
   if (threadIdx.x == 0 && jb.prof) atomicAdd(&jb.prof[slot], (unsigned long long)v);
 }
 
+constexpr int kTileElems = 2 * TK * TLD;                                // GEMM staging tiles
+constexpr int kQrSmemElems = (3 * JB + 1) * 128 - kTileElems;           // rest of the dynamic smem
+
 struct Ctx {
   const Job* job;
   double2* mps;
@@ -1329,7 +1332,8 @@ __device__ void move_right(const Ctx& cx, Smem& sm, int c) {
   const int Mx = 2 * cl, Nx = cr, N2 = 2 * cr2;
   double2* S = cx.site(c);
   double2* T = cx.site(c + 1);
-  double2* W = cx.W;
+  // the QR runs in shared memory when the site matrix fits beside the GEMM tiles
+  double2* W = (Mx * Nx <= kQrSmemElems) ? cx.tile + kTileElems : cx.W;
   double2* R = cx.X;
   double2* T0 = cx.W0;
   for (int e = threadIdx.x; e < Mx * Nx; e += NT) {
@@ -1367,7 +1371,8 @@ __device__ void move_left(const Ctx& cx, Smem& sm, int c) {
   const int Mx = 2 * cr, Nx = cl, Mp = 2 * clm;
   double2* S = cx.site(c);
   double2* T = cx.site(c - 1);
-  double2* W = cx.W;
+  // the QR runs in shared memory when the site matrix fits beside the GEMM tiles
+  double2* W = (Mx * Nx <= kQrSmemElems) ? cx.tile + kTileElems : cx.W;
   double2* R = cx.X;
   double2* T0 = cx.W0;
   for (int e = threadIdx.x; e < Nx * Mx; e += NT) {

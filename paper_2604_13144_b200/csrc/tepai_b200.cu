@@ -798,9 +798,14 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   int sweep = 0;
   bool conv = false;
   for (; sweep < MAXSWEEP; ++sweep) {
+    const long long ts0 = prof_clock();
     J.refresh_norms(sm, tol, sweep == 0);
     J.sweep(sm);
     __syncthreads();
+    if (threadIdx.x == 0 && sm.prof && Mw == 128 && sweep < 16) {
+      atomicAdd(&sm.prof[40 + sweep], (unsigned long long)(prof_clock() - ts0));
+      atomicAdd(&sm.prof[56 + min(sweep, 7)], 1ull);
+    }
     if (sm.flag == 0 || sm.offmax < 1e-16 * TB_TOLSCALE) {
       conv = true;
       break;

@@ -118,9 +118,9 @@ struct Smem {
   int dims[MAXN + 1];
   double sig[MAXDIM];
   double nrm[4 * 32];
-  double pbuf[NWARP][2][6];  // per-warp Jacobi parameter exchange
+  double dsc[4 * 32];        // Jacobi column scales (true column = dsc * stored)
   double wbest[32];          // per-half-warp pivot candidates (QRCP)
-  int qcnt[32];              // cross-phase Q visit counters
+  int qcnt[3 * 32];          // cross-phase Q visit counters (per slot, column)
   unsigned char chg[4 * 32]; // bit0: rotated in the previous sweep, bit1: in this sweep
   int jncol[4];              // live columns per Jacobi block slot
   int wbidx[32];
@@ -368,7 +368,7 @@ __device__ __forceinline__ void sts2(uint32_t a, double2 v) {
 
 // Rotation of one pair.  Identity when s == 0 (c = 1, e = 1).
 struct Rot {
-  double c, s, er, ei, tg;
+  double c, s, er, ei, tg, t;
 };
 __device__ __forceinline__ void atomic_max_pos(double* a, double v) {  // v >= 0
   atomicMax((unsigned long long*)a, (unsigned long long)__double_as_longlong(v));
@@ -418,6 +418,7 @@ __device__ __forceinline__ Rot rot_params(double gr, double gi, double al, doubl
   p.er = rot ? gr * ig : 1.0;
   p.ei = rot ? -gi * ig : 0.0;
   p.tg = rot ? t * g : 0.0;
+  p.t = rot ? t : 0.0;
   return p;
 }
 
@@ -468,20 +469,31 @@ __device__ __forceinline__ void hcol_stg(double2* p, const HCol<HR>& c, int Mw) 
   }
 }
 
+// Scaled ("fast") rotation of one pair.  Columns are stored as a = da * A,
+// b = db * B with real scales, and the unitary update
+//   a' = c (a - t E b),  b' = c (b + t conj(E) a)
+// becomes A' = A - f1 B, B' = B + f2 A with f1 = t E db/da, f2 = t conj(E) da/db
+// while the factor c moves into the scales (da' = c da, db' = c db): 8 DFMA
+// per complex row pair instead of 12.
 template <int HR>
-__device__ __forceinline__ void apply_rot(HCol<HR>& a, HCol<HR>& b, const Rot& p) {
-  const double sre = p.s * p.er, sim = p.s * p.ei, cre = p.c * p.er, cim = p.c * p.ei;
+__device__ __forceinline__ void apply_rot_s(HCol<HR>& a, HCol<HR>& b, double f1r, double f1i, double f2r,
+                                            double f2i) {
 #pragma unroll
   for (int q = 0; q < HR; ++q) {
     const double2 x = a.v[q], y = b.v[q];
-    double2 na, nb;
-    na.x = fma(sim, y.y, fma(-sre, y.x, p.c * x.x));
-    na.y = fma(-sim, y.x, fma(-sre, y.y, p.c * x.y));
-    nb.x = fma(-cim, y.y, fma(cre, y.x, p.s * x.x));
-    nb.y = fma(cim, y.x, fma(cre, y.y, p.s * x.y));
-    a.v[q] = na;
-    b.v[q] = nb;
+    a.v[q].x = fma(-f1r, y.x, fma(f1i, y.y, x.x));
+    a.v[q].y = fma(-f1r, y.y, fma(-f1i, y.x, x.y));
+    b.v[q].x = fma(f2r, x.x, fma(-f2i, x.y, y.x));
+    b.v[q].y = fma(f2r, x.y, fma(f2i, x.x, y.y));
   }
+}
+
+__device__ __forceinline__ double rcp_acc(double x) {  // ~1 ulp
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
 }
 
 __device__ __forceinline__ double half_sum(double v) {
@@ -492,12 +504,13 @@ __device__ __forceinline__ double half_sum(double v) {
   return v;
 }
 
-// one pair per half-warp; `valid` may differ between the halves.  Returns
-// whether THIS half rotated.  Branches are warp-uniform (both halves take
-// the apply path if either rotates; a non-rotating half applies identity).
+// one pair per half-warp; `valid` may differ between the halves.  na / nb are
+// the TRUE squared norms, da / db the column scales.  Returns whether THIS
+// half rotated.  Branches are warp-uniform (a non-rotating half applies the
+// exact identity: f1 = f2 = 0, c = 1).
 template <int HR>
-__device__ __forceinline__ bool rot_half(HCol<HR>& a, HCol<HR>& b, double& na, double& nb, bool valid, double tol2,
-                                         double& offmax) {
+__device__ __forceinline__ bool rot_half(HCol<HR>& a, HCol<HR>& b, double& na, double& nb, double& da, double& db,
+                                         bool valid, double tol2, double& offmax) {
   double2 g = cz(), h = cz();
 #pragma unroll
   for (int q = 0; q < HR; q += 2) {
@@ -507,11 +520,24 @@ __device__ __forceinline__ bool rot_half(HCol<HR>& a, HCol<HR>& b, double& na, d
   double gr = g.x + h.x, gi = g.y + h.y;
   gr = half_sum(gr);
   gi = half_sum(gi);
+  const double dd = da * db;
+  gr *= dd;
+  gi *= dd;
   const Rot p = rot_params(gr, gi, na, nb, valid, tol2);
   const bool mine = p.s != 0.0;
-  if (mine) offmax = fmax(offmax, fma(gr, gr, gi * gi) / (na * nb));
-  if (__any_sync(0xffffffffu, mine)) apply_rot(a, b, p);
+  if (mine) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(na * nb));
+    offmax = fmax(offmax, fma(gr, gr, gi * gi) * r);
+  }
   const double nan_ = na - p.tg, nbn = nb + p.tg;
+  if (__any_sync(0xffffffffu, mine)) {
+    const double inv = rcp_acc(dd);
+    const double r1 = p.t * db * db * inv, r2 = p.t * da * da * inv;
+    apply_rot_s(a, b, p.er * r1, p.ei * r1, p.er * r2, -p.ei * r2);
+    da *= p.c;
+    db *= p.c;
+  }
   const bool fa = mine && nan_ < 0.5 * na, fb = mine && nbn < 0.5 * nb;
   na = nan_;
   nb = nbn;
@@ -522,8 +548,8 @@ __device__ __forceinline__ bool rot_half(HCol<HR>& a, HCol<HR>& b, double& na, d
       ea += abs2(a.v[q]);
       eb += abs2(b.v[q]);
     }
-    ea = half_sum(ea);
-    eb = half_sum(eb);
+    ea = half_sum(ea) * (da * da);
+    eb = half_sum(eb) * (db * db);
     if (fa) na = ea;
     if (fb) nb = eb;
   }
@@ -567,17 +593,15 @@ struct JacobiH {
           }
         }
         if (!__any_sync(0xffffffffu, valid)) continue;
+        // unconditional loads: slot columns past the live count are zeros
+        // and a non-rotating half applies the exact identity
         HCol<HR> a, b;
         const uint32_t ai = scol(s, i), aj = scol(s, j);
-        if (valid) {
-          hcol_lds(a, ai);
-          hcol_lds(b, aj);
-        } else {
-#pragma unroll
-          for (int q = 0; q < HR; ++q) a.v[q] = b.v[q] = cz();
-        }
+        hcol_lds(a, ai);
+        hcol_lds(b, aj);
         double na = valid ? sm.nrm[s * JB + i] : 0.0, nb = valid ? sm.nrm[s * JB + j] : 0.0;
-        const bool rr = rot_half<HR>(a, b, na, nb, valid, tol2, offmax);
+        double da = sm.dsc[s * JB + i], db = sm.dsc[s * JB + j];
+        const bool rr = rot_half<HR>(a, b, na, nb, da, db, valid, tol2, offmax);
         if (rr) {
           any = true;
           hcol_sts(ai, a);
@@ -585,6 +609,8 @@ struct JacobiH {
           if (hl == 0) {
             sm.nrm[s * JB + i] = na;
             sm.nrm[s * JB + j] = nb;
+            sm.dsc[s * JB + i] = da;
+            sm.dsc[s * JB + j] = db;
             sm.chg[s * JB + i] |= 2;
             sm.chg[s * JB + j] |= 2;
           }
@@ -596,69 +622,105 @@ struct JacobiH {
   }
 
   // P column of half k (slot sp) against the Q columns of smem slot sq
-  __device__ void cross(HCol<HR>& pc, double& np, int nP, int sp, int sq, Smem& sm) {
+  // P column of half k (slot sp) against the Q columns of up to three smem
+  // slots sq0..sq{S-1}.  Visit (m, x) (round S*m + x): half k takes column
+  // (k + m) mod 32 of slot x.  A Q column is therefore touched every S rounds
+  // (by halves k, k-1, ...), so with S > 1 the halves may drift apart by S
+  // rounds instead of running in lockstep — their latency-bound stretches
+  // (reductions, rotation parameters) then overlap other halves' FP64 work.
+  __device__ void cross(HCol<HR>& pc, double& np, double& dp, int nP, int sp, int sq0, int sq1, int sq2, int S,
+                        Smem& sm) {
     const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
-    const int nQ = sm.jncol[sq];
     const bool vp = hw < nP;
     bool any = false;
-    if (threadIdx.x < 32) sm.qcnt[threadIdx.x] = 0;
+    if (threadIdx.x < 3 * 32) sm.qcnt[threadIdx.x] = 0;
     __syncthreads();
     const long long tc0 = prof_clock();
-    for (int r = 0; r < 32; ++r) {
-      const int c = (hw + r) & 31;  // Q column handled by this half in round r
-      if (r > 0) {
-        if (hl == 0)
-          while (*(volatile int*)&sm.qcnt[c] < r) {}
-        __syncwarp();
-        __threadfence_block();
-      }
-      const bool valid = vp && c < nQ && ((sm.chg[sp * JB + hw] | sm.chg[sq * JB + c]) & 1);
-      if (__any_sync(0xffffffffu, valid)) {
-        HCol<HR> q;
-        const uint32_t aq = scol(sq, c);
-        if (valid) hcol_lds(q, aq);
-        else {
-#pragma unroll
-          for (int k = 0; k < HR; ++k) q.v[k] = cz();
+    for (int m = 0; m < 32; ++m) {
+      const int c = (hw + m) & 31;  // Q column handled by this half in visit m
+      for (int x = 0; x < S; ++x) {
+        const int sq = x == 0 ? sq0 : (x == 1 ? sq1 : sq2);
+        int* cnt = &sm.qcnt[x * 32 + c];
+        if (m > 0) {
+          if (hl == 0)
+            while (*(volatile int*)cnt < m) {}
+          __syncwarp();
+          __threadfence_block();
         }
-        double nq = valid ? sm.nrm[sq * JB + c] : 0.0;
-        const double npo = np;
-        const bool rr = rot_half<HR>(pc, q, np, nq, valid, tol2, offmax);
-        if (!valid) np = npo;
-        if (rr) {
-          any = true;
-          hcol_sts(aq, q);
-          if (hl == 0) {
-            sm.nrm[sq * JB + c] = nq;
-            sm.chg[sp * JB + hw] |= 2;
-            sm.chg[sq * JB + c] |= 2;
+        const bool valid = vp && c < sm.jncol[sq] && ((sm.chg[sp * JB + hw] | sm.chg[sq * JB + c]) & 1);
+        if (__any_sync(0xffffffffu, valid)) {
+          HCol<HR> q;
+          const uint32_t aq = scol(sq, c);
+          hcol_lds(q, aq);  // unconditional (see within)
+          double nq = valid ? sm.nrm[sq * JB + c] : 0.0, dq = sm.dsc[sq * JB + c];
+          const double npo = np;
+          const bool rr = rot_half<HR>(pc, q, np, nq, dp, dq, valid, tol2, offmax);
+          if (!valid) np = npo;
+          if (rr) {
+            any = true;
+            hcol_sts(aq, q);
+            if (hl == 0) {
+              sm.nrm[sq * JB + c] = nq;
+              sm.dsc[sq * JB + c] = dq;
+              sm.chg[sp * JB + hw] |= 2;
+              sm.chg[sq * JB + c] |= 2;
+            }
           }
         }
+        __threadfence_block();
+        __syncwarp();
+        if (hl == 0) *(volatile int*)cnt = m + 1;
       }
-      __threadfence_block();
-      __syncwarp();
-      if (hl == 0) *(volatile int*)&sm.qcnt[c] = r + 1;
     }
     __syncthreads();
     if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
     if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[14], (unsigned long long)(prof_clock() - tc0));
   }
 
-  __device__ void load_p(HCol<HR>& pc, double& np, int s, Smem& sm) {
+  __device__ void load_p(HCol<HR>& pc, double& np, double& dp, int s, Smem& sm) {
     const int hw = threadIdx.x >> 4;
     if (s < 3) hcol_lds(pc, scol(s, hw));
     else hcol_ldg(pc, G + (size_t)hw * Mw, Mw);
     np = sm.nrm[s * JB + hw];
+    dp = sm.dsc[s * JB + hw];
   }
-  __device__ void store_p(const HCol<HR>& pc, double np, int s, Smem& sm) {
+  __device__ void store_p(const HCol<HR>& pc, double np, double dp, int s, Smem& sm) {
     const int hw = threadIdx.x >> 4;
     if (s < 3) hcol_sts(scol(s, hw), pc);
     else hcol_stg(G + (size_t)hw * Mw, pc, Mw);
-    if ((threadIdx.x & 15) == 0) sm.nrm[s * JB + hw] = np;
+    if ((threadIdx.x & 15) == 0) {
+      sm.nrm[s * JB + hw] = np;
+      sm.dsc[s * JB + hw] = dp;
+    }
+  }
+
+  // multiply every stored column by its scale and reset the scales to 1
+  __device__ void fold_scales(Smem& sm, bool first) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (!first) {
+      for (int c = warp; c < JB * nblk; c += NWARP) {
+        const double d = sm.dsc[c];
+        if (d == 1.0) continue;
+        const int s = c / JB, k = c - s * JB;
+        if (s < 3) {
+          for (int y = lane; y < LD; y += 32) {
+            const uint32_t a = scol(s, k) + 16u * y;
+            sts2(a, cscale(lds2(a), d));
+          }
+        } else {
+          double2* p = G + (size_t)k * Mw;
+          for (int y = lane; y < Mw; y += 32) p[y] = cscale(p[y], d);
+        }
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < JB * nblk; c += NT) sm.dsc[c] = 1.0;
+    __syncthreads();
   }
 
   __device__ void refresh_norms(Smem& sm, double tol, bool first) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    fold_scales(sm, first);
     for (int c = warp; c < JB * nblk; c += NWARP) {
       const int s = c / JB, k = c - s * JB;
       double acc = 0.0;
@@ -708,20 +770,20 @@ struct JacobiH {
     within(0, 1, 2, nsm, sm);
     if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[13], (unsigned long long)(prof_clock() - tw0));
     HCol<HR> pc;
-    double np;
+    double np, dp;
     if (nblk == 4) {
-      load_p(pc, np, 3, sm);
-      for (int s = 0; s < 3; ++s) cross(pc, np, sm.jncol[3], 3, s, sm);
+      load_p(pc, np, dp, 3, sm);
+      cross(pc, np, dp, sm.jncol[3], 3, 0, 1, 2, 3, sm);
       // swap contents of A and G (P holds the current G columns)
       {
         HCol<HR> t;
-        double nt;
-        load_p(t, nt, 0, sm);
+        double nt, dt;
+        load_p(t, nt, dt, 0, sm);
         const int hw = threadIdx.x >> 4;
         unsigned char fa = sm.chg[hw], fg = sm.chg[3 * JB + hw];
         __syncthreads();
-        store_p(pc, np, 0, sm);
-        store_p(t, nt, 3, sm);
+        store_p(pc, np, dp, 0, sm);
+        store_p(t, nt, dt, 3, sm);
         if ((threadIdx.x & 15) == 0) {
           sm.chg[hw] = fg;
           sm.chg[3 * JB + hw] = fa;
@@ -735,20 +797,19 @@ struct JacobiH {
         __syncthreads();
       }
       within(0, 0, 0, 1, sm);
-      load_p(pc, np, 3, sm);
-      cross(pc, np, sm.jncol[3], 3, 1, sm);
-      cross(pc, np, sm.jncol[3], 3, 2, sm);
-      store_p(pc, np, 3, sm);
+      load_p(pc, np, dp, 3, sm);
+      cross(pc, np, dp, sm.jncol[3], 3, 1, 2, 2, 2, sm);
+      store_p(pc, np, dp, 3, sm);
       __syncthreads();
-      load_p(pc, np, 1, sm);
-      cross(pc, np, sm.jncol[1], 1, 2, sm);
-      store_p(pc, np, 1, sm);
+      load_p(pc, np, dp, 1, sm);
+      cross(pc, np, dp, sm.jncol[1], 1, 2, 2, 2, 1, sm);
+      store_p(pc, np, dp, 1, sm);
       __syncthreads();
     } else {
       for (int sp = 0; sp + 1 < nsm; ++sp) {
-        load_p(pc, np, sp, sm);
-        for (int sq = sp + 1; sq < nsm; ++sq) cross(pc, np, sm.jncol[sp], sp, sq, sm);
-        store_p(pc, np, sp, sm);
+        load_p(pc, np, dp, sp, sm);
+        cross(pc, np, dp, sm.jncol[sp], sp, sp + 1, sp + 2, sp + 2, nsm - 1 - sp, sm);
+        store_p(pc, np, dp, sp, sm);
         __syncthreads();
       }
     }
@@ -813,6 +874,7 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     __syncthreads();
   }
   if (threadIdx.x == 0) sm.sweeps = sweep + 1;
+  J.fold_scales(sm, false);
   for (int e = threadIdx.x; e < nsm * JB * Mw; e += NT) {
     const int c = e / Mw, y = e - c * Mw;
     W[(size_t)c * Mw + y] = smem[(size_t)c * LD + y];

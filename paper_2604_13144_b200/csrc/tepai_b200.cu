@@ -474,17 +474,24 @@ __device__ __forceinline__ void hcol_stg(double2* p, const HCol<HR>& c, int Mw) 
 //   a' = c (a - t E b),  b' = c (b + t conj(E) a)
 // becomes A' = A - f1 B, B' = B + f2 A with f1 = t E db/da, f2 = t conj(E) da/db
 // while the factor c moves into the scales (da' = c da, db' = c db): 8 DFMA
-// per complex row pair instead of 12.
-template <int HR>
-__device__ __forceinline__ void apply_rot_s(HCol<HR>& a, HCol<HR>& b, double f1r, double f1i, double f2r,
-                                            double f2i) {
+// per complex row pair instead of 12.  B' goes straight to shared memory
+// (predicated on `st`); A' is either kept in registers (KEEP_A, the resident
+// P column of a cross phase) or stored as well.
+template <int HR, bool KEEP_A>
+__device__ __forceinline__ void apply_rot_s(HCol<HR>& a, const HCol<HR>& b, uint32_t sa, uint32_t sb, bool st,
+                                            double f1r, double f1i, double f2r, double f2i) {
+  const uint32_t l = (threadIdx.x & 15) * 16u;
 #pragma unroll
   for (int q = 0; q < HR; ++q) {
     const double2 x = a.v[q], y = b.v[q];
-    a.v[q].x = fma(-f1r, y.x, fma(f1i, y.y, x.x));
-    a.v[q].y = fma(-f1r, y.y, fma(-f1i, y.x, x.y));
-    b.v[q].x = fma(f2r, x.x, fma(-f2i, x.y, y.x));
-    b.v[q].y = fma(f2r, x.y, fma(f2i, x.x, y.y));
+    double2 nb, na;
+    nb.x = fma(f2r, x.x, fma(-f2i, x.y, y.x));
+    nb.y = fma(f2r, x.y, fma(f2i, x.x, y.y));
+    na.x = fma(-f1r, y.x, fma(f1i, y.y, x.x));
+    na.y = fma(-f1r, y.y, fma(-f1i, y.x, x.y));
+    if (st) sts2(sb + l + 256u * q, nb);
+    if (KEEP_A) a.v[q] = na;
+    else if (st) sts2(sa + l + 256u * q, na);
   }
 }
 
@@ -505,12 +512,14 @@ __device__ __forceinline__ double half_sum(double v) {
 }
 
 // one pair per half-warp; `valid` may differ between the halves.  na / nb are
-// the TRUE squared norms, da / db the column scales.  Returns whether THIS
-// half rotated.  Branches are warp-uniform (a non-rotating half applies the
-// exact identity: f1 = f2 = 0, c = 1).
-template <int HR>
-__device__ __forceinline__ bool rot_half(HCol<HR>& a, HCol<HR>& b, double& na, double& nb, double& da, double& db,
-                                         bool valid, double tol2, double& offmax) {
+// the TRUE squared norms, da / db the column scales; sa / sb the shared-memory
+// homes of the two columns (written only when THIS half rotates).  Returns
+// whether this half rotated.  Branches are warp-uniform (a non-rotating half
+// applies the exact identity: f1 = f2 = 0, c = 1, and stores nothing).
+template <int HR, bool KEEP_A>
+__device__ __forceinline__ bool rot_half(HCol<HR>& a, const HCol<HR>& b, uint32_t sa, uint32_t sb, double& na,
+                                         double& nb, double& da, double& db, bool valid, double tol2,
+                                         double& offmax) {
   double2 g = cz(), h = cz();
 #pragma unroll
   for (int q = 0; q < HR; q += 2) {
@@ -534,19 +543,20 @@ __device__ __forceinline__ bool rot_half(HCol<HR>& a, HCol<HR>& b, double& na, d
   if (__any_sync(0xffffffffu, mine)) {
     const double inv = rcp_acc(dd);
     const double r1 = p.t * db * db * inv, r2 = p.t * da * da * inv;
-    apply_rot_s(a, b, p.er * r1, p.ei * r1, p.er * r2, -p.ei * r2);
+    apply_rot_s<HR, KEEP_A>(a, b, sa, sb, mine, p.er * r1, p.ei * r1, p.er * r2, -p.ei * r2);
     da *= p.c;
     db *= p.c;
   }
   const bool fa = mine && nan_ < 0.5 * na, fb = mine && nbn < 0.5 * nb;
   na = nan_;
   nb = nbn;
-  if (__any_sync(0xffffffffu, fa || fb)) {
+  if (__any_sync(0xffffffffu, fa || fb)) {  // cancellation: exact norms of the new columns
+    const uint32_t l = (threadIdx.x & 15) * 16u;
     double ea = 0.0, eb = 0.0;
 #pragma unroll
     for (int q = 0; q < HR; ++q) {
-      ea += abs2(a.v[q]);
-      eb += abs2(b.v[q]);
+      ea += abs2(KEEP_A ? a.v[q] : lds2(sa + l + 256u * q));
+      eb += abs2(lds2(sb + l + 256u * q));
     }
     ea = half_sum(ea) * (da * da);
     eb = half_sum(eb) * (db * db);
@@ -567,7 +577,12 @@ struct JacobiH {
 
   __device__ uint32_t scol(int s, int c) const { return base + (uint32_t)(s * JB + c) * CB; }
 
-  // round robin inside up to three smem slots; pairs are dealt to halves
+  // Round robin inside up to three smem slots.  The slot-rounds are
+  // enumerated as m = round * ns + slot and each CTA-wide step takes two of
+  // them (halves 0-15: m = 2k, halves 16-31: m = 2k + 1; a slot-round has at
+  // most 16 pairs).  For ns >= 2 the two slot-rounds of a step touch
+  // different slots, and a slot's consecutive rounds (m, m + ns) always fall
+  // in different steps, so one barrier per step orders everything.
   __device__ void within(int s0, int s1, int s2, int ns, Smem& sm) {
     const int hw = threadIdx.x >> 4;  // half-warp id 0..31
     const int hl = threadIdx.x & 15;
@@ -576,39 +591,37 @@ struct JacobiH {
       const int nb = sm.jncol[x == 0 ? s0 : (x == 1 ? s1 : s2)];
       rounds = max(rounds, nb + (nb & 1) - 1);
     }
-    for (int r = 0; r < rounds; ++r) {
-      bool any = false;
-      // 16 pairs per slot and round at most: pair (x, p) -> half x*16+p (mod 32)
-      for (int f0 = 0; f0 < 3 * 16; f0 += 32) {
-        const int f = f0 + hw;
-        const int x = f >> 4, p = f & 15;
-        bool valid = false;
-        int s = 0, i = 0, j = 0;
-        if (x < ns) {
-          s = (x == 0) ? s0 : (x == 1 ? s1 : s2);
-          const int nb = sm.jncol[s], nbp = nb + (nb & 1);
-          if (r < nbp - 1 && p < nbp / 2) {
-            rr_pair(r, p, nbp, i, j);
-            valid = i < nb && j < nb && ((sm.chg[s * JB + i] | sm.chg[s * JB + j]) & 1);
-          }
+    const int per = ns >= 2 ? 2 : 1;
+    const int nsteps = (rounds * ns + per - 1) / per;
+    bool any = false;
+    for (int k = 0; k < nsteps; ++k) {
+      const int m = per * k + (hw >> 4), p = hw & 15;
+      const int r = m / ns, x = m - r * ns;
+      bool valid = false;
+      int s = 0, i = 0, j = 0;
+      if ((hw >> 4) < per && r < rounds) {
+        s = (x == 0) ? s0 : (x == 1 ? s1 : s2);
+        const int nb = sm.jncol[s], nbp = nb + (nb & 1);
+        if (r < nbp - 1 && p < nbp / 2) {
+          rr_pair(r, p, nbp, i, j);
+          valid = i < nb && j < nb && ((sm.chg[s * JB + i] | sm.chg[s * JB + j]) & 1);
         }
-        if (!__any_sync(0xffffffffu, valid)) continue;
+      }
+      if (__any_sync(0xffffffffu, valid)) {
         // unconditional loads: slot columns past the live count are zeros
         // and a non-rotating half applies the exact identity
         HCol<HR> a, b;
         const uint32_t ai = scol(s, i), aj = scol(s, j);
         hcol_lds(a, ai);
         hcol_lds(b, aj);
-        double na = valid ? sm.nrm[s * JB + i] : 0.0, nb = valid ? sm.nrm[s * JB + j] : 0.0;
+        double na = valid ? sm.nrm[s * JB + i] : 0.0, nb2 = valid ? sm.nrm[s * JB + j] : 0.0;
         double da = sm.dsc[s * JB + i], db = sm.dsc[s * JB + j];
-        const bool rr = rot_half<HR>(a, b, na, nb, da, db, valid, tol2, offmax);
+        const bool rr = rot_half<HR, false>(a, b, ai, aj, na, nb2, da, db, valid, tol2, offmax);
         if (rr) {
           any = true;
-          hcol_sts(ai, a);
-          hcol_sts(aj, b);
           if (hl == 0) {
             sm.nrm[s * JB + i] = na;
-            sm.nrm[s * JB + j] = nb;
+            sm.nrm[s * JB + j] = nb2;
             sm.dsc[s * JB + i] = da;
             sm.dsc[s * JB + j] = db;
             sm.chg[s * JB + i] |= 2;
@@ -616,12 +629,12 @@ struct JacobiH {
           }
         }
       }
-      if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
       __syncthreads();
     }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
+    __syncthreads();
   }
 
-  // P column of half k (slot sp) against the Q columns of smem slot sq
   // P column of half k (slot sp) against the Q columns of up to three smem
   // slots sq0..sq{S-1}.  Visit (m, x) (round S*m + x): half k takes column
   // (k + m) mod 32 of slot x.  A Q column is therefore touched every S rounds
@@ -654,11 +667,10 @@ struct JacobiH {
           hcol_lds(q, aq);  // unconditional (see within)
           double nq = valid ? sm.nrm[sq * JB + c] : 0.0, dq = sm.dsc[sq * JB + c];
           const double npo = np;
-          const bool rr = rot_half<HR>(pc, q, np, nq, dp, dq, valid, tol2, offmax);
+          const bool rr = rot_half<HR, true>(pc, q, 0u, aq, np, nq, dp, dq, valid, tol2, offmax);
           if (!valid) np = npo;
           if (rr) {
             any = true;
-            hcol_sts(aq, q);
             if (hl == 0) {
               sm.nrm[sq * JB + c] = nq;
               sm.dsc[sq * JB + c] = dq;

@@ -117,15 +117,15 @@ struct Job {
 struct Smem {
   int dims[MAXN + 1];
   double sig[MAXDIM];
-  double nrm[4 * 32];
-  double dsc[4 * 32];        // Jacobi column scales (true column = dsc * stored)
+  double nrm[MAXDIM];
+  double dsc[MAXDIM];        // Jacobi column scales (true column = dsc * stored)
   double wbest[32];          // per-half-warp pivot candidates (QRCP)
   int qcnt[3 * 32];          // cross-phase Q visit counters (per slot, column)
-  unsigned char chg[4 * 32]; // bit0: rotated in the previous sweep, bit1: in this sweep
+  unsigned char chg[MAXDIM]; // bit0: rotated in the previous sweep, bit1: in this sweep
   int jncol[4];              // live columns per Jacobi block slot
   int wbidx[32];
-  double nref[4 * 32];
-  int qperm[4 * 32];
+  double nref[MAXDIM];
+  int qperm[MAXDIM];
   int qpinv[MAXDIM];
   int perm[MAXDIM];
   double2 rco[MAXDIM];
@@ -896,6 +896,327 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   return conv ? neff : -neff;
 }
 
+// ----------------------------------------------------------------------------
+// Wide Jacobi (Mw <= 256 rows, Nw <= 256 columns: the chi = 128 problems).
+// A column is 256 rows = 4 KB, so only one block of 32 columns fits in shared
+// memory.  The columns stay in global memory (L2) in blocks of <= 32; a sweep
+// takes every block once as the register-resident P block (one column per
+// half-warp, 16 lanes x 16 rows) and streams the later blocks through the
+// shared-memory slot as Q (same counter-ordered cross phase as JacobiH), plus
+// a round robin inside each block.  Shared-memory columns are streamed in
+// row chunks (4 rows per lane) so a pair never holds two full columns in
+// registers.  Same scaled rotations, convergence test and dead-column rule
+// as the half-warp Jacobi.
+// ----------------------------------------------------------------------------
+struct JacobiW {
+  static constexpr int HR = 16, CH = 4;     // rows per lane, rows per streamed chunk
+  static constexpr int LD = 16 * HR;        // 256 padded rows per smem column
+  static constexpr uint32_t CB = LD * 16u;  // bytes per smem column
+  uint32_t base;
+  double2* W;
+  int Mw, Nw, nblk;
+  int start[9], ncl[8];
+  double tol2, offmax;
+
+  __device__ uint32_t scol(int c) const { return base + (uint32_t)c * CB; }
+  __device__ uint32_t lrow() const { return (threadIdx.x & 15) * 16u; }
+
+  __device__ void stage(int b) {
+    const int nc = ncl[b], c0 = start[b];
+    for (int e = threadIdx.x; e < JB * LD; e += NT) {
+      const int c = e / LD, y = e - c * LD;
+      const double2 v = (c < nc && y < Mw) ? W[(size_t)(c0 + c) * Mw + y] : cz();
+      sts2(scol(c) + 16u * y, v);
+    }
+    __syncthreads();
+  }
+  __device__ void unstage(int b) {
+    const int nc = ncl[b], c0 = start[b];
+    for (int e = threadIdx.x; e < nc * Mw; e += NT) {
+      const int c = e / Mw, y = e - c * Mw;
+      W[(size_t)(c0 + c) * Mw + y] = lds2(scol(c) + 16u * y);
+    }
+    __syncthreads();
+  }
+
+  // rotation of the pair (a, b); a in registers (KEEP_A) or in smem at sa,
+  // b in smem at sb.  na/nb true squared norms, da/db scales.
+  template <bool A_REG>
+  __device__ __forceinline__ bool rot(HCol<HR>& a, uint32_t sa, uint32_t sb, double& na, double& nb, double& da,
+                                      double& db, bool valid) {
+    const uint32_t l = lrow();
+    double2 g = cz(), h = cz();
+#pragma unroll
+    for (int q0 = 0; q0 < HR; q0 += CH) {
+      double2 x[CH], y[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        x[q] = A_REG ? a.v[q0 + q] : lds2(sa + l + 256u * (q0 + q));
+        y[q] = lds2(sb + l + 256u * (q0 + q));
+      }
+#pragma unroll
+      for (int q = 0; q < CH; q += 2) {
+        cfmac(g, x[q], y[q]);
+        cfmac(h, x[q + 1], y[q + 1]);
+      }
+    }
+    double gr = half_sum(g.x + h.x), gi = half_sum(g.y + h.y);
+    const double dd = da * db;
+    gr *= dd;
+    gi *= dd;
+    const Rot p = rot_params(gr, gi, na, nb, valid, tol2);
+    const bool mine = p.s != 0.0;
+    if (mine) {
+      double r;
+      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(na * nb));
+      offmax = fmax(offmax, fma(gr, gr, gi * gi) * r);
+    }
+    const double nan_ = na - p.tg, nbn = nb + p.tg;
+    if (__any_sync(0xffffffffu, mine)) {
+      const double inv = rcp_acc(dd);
+      const double r1 = p.t * db * db * inv, r2 = p.t * da * da * inv;
+      const double f1r = p.er * r1, f1i = p.ei * r1, f2r = p.er * r2, f2i = -p.ei * r2;
+#pragma unroll
+      for (int q0 = 0; q0 < HR; q0 += CH) {
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const uint32_t o = l + 256u * (q0 + q);
+          const double2 x = A_REG ? a.v[q0 + q] : lds2(sa + o);
+          const double2 y = lds2(sb + o);
+          double2 nx, ny;
+          ny.x = fma(f2r, x.x, fma(-f2i, x.y, y.x));
+          ny.y = fma(f2r, x.y, fma(f2i, x.x, y.y));
+          nx.x = fma(-f1r, y.x, fma(f1i, y.y, x.x));
+          nx.y = fma(-f1r, y.y, fma(-f1i, y.x, x.y));
+          if (mine) sts2(sb + o, ny);
+          if (A_REG) a.v[q0 + q] = nx;
+          else if (mine) sts2(sa + o, nx);
+        }
+      }
+      da *= p.c;
+      db *= p.c;
+    }
+    const bool fa = mine && nan_ < 0.5 * na, fb = mine && nbn < 0.5 * nb;
+    na = nan_;
+    nb = nbn;
+    if (__any_sync(0xffffffffu, fa || fb)) {
+      double ea = 0.0, eb = 0.0;
+#pragma unroll
+      for (int q = 0; q < HR; ++q) {
+        ea += abs2(A_REG ? a.v[q] : lds2(sa + l + 256u * q));
+        eb += abs2(lds2(sb + l + 256u * q));
+      }
+      ea = half_sum(ea) * (da * da);
+      eb = half_sum(eb) * (db * db);
+      if (fa) na = ea;
+      if (fb) nb = eb;
+    }
+    return mine;
+  }
+
+  // round robin inside the staged block b (16 pairs per round at most)
+  __device__ void within(int b, Smem& sm) {
+    const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
+    const int nb = ncl[b], nbp = nb + (nb & 1), c0 = start[b];
+    bool any = false;
+    for (int r = 0; r < nbp - 1; ++r) {
+      int i = 0, j = 0;
+      bool valid = false;
+      if (hw < nbp / 2) {
+        rr_pair(r, hw, nbp, i, j);
+        valid = i < nb && j < nb && ((sm.chg[c0 + i] | sm.chg[c0 + j]) & 1);
+      }
+      if (__any_sync(0xffffffffu, valid)) {
+        HCol<HR> dummy;
+        double na = valid ? sm.nrm[c0 + i] : 0.0, nb2 = valid ? sm.nrm[c0 + j] : 0.0;
+        double da = sm.dsc[c0 + i], db = sm.dsc[c0 + j];
+        if (rot<false>(dummy, scol(i), scol(j), na, nb2, da, db, valid)) {
+          any = true;
+          if (hl == 0) {
+            sm.nrm[c0 + i] = na;
+            sm.nrm[c0 + j] = nb2;
+            sm.dsc[c0 + i] = da;
+            sm.dsc[c0 + j] = db;
+            sm.chg[c0 + i] |= 2;
+            sm.chg[c0 + j] |= 2;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
+  }
+
+  // P block bp (one column per half, in registers) against staged block bq
+  __device__ void cross(HCol<HR>& pc, double& np, double& dp, int bp, int bq, Smem& sm) {
+    const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
+    const int nP = ncl[bp], nQ = ncl[bq], p0 = start[bp], q0 = start[bq];
+    const bool vp = hw < nP;
+    bool any = false;
+    if (threadIdx.x < 32) sm.qcnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int r = 0; r < 32; ++r) {
+      const int c = (hw + r) & 31;
+      if (r > 0) {
+        if (hl == 0)
+          while (*(volatile int*)&sm.qcnt[c] < r) {}
+        __syncwarp();
+        __threadfence_block();
+      }
+      const bool valid = vp && c < nQ && ((sm.chg[p0 + hw] | sm.chg[q0 + c]) & 1);
+      if (__any_sync(0xffffffffu, valid)) {
+        double nq = valid ? sm.nrm[q0 + c] : 0.0, dq = c < nQ ? sm.dsc[q0 + c] : 1.0;
+        const double npo = np;
+        const bool rr = rot<true>(pc, 0u, scol(c), np, nq, dp, dq, valid);
+        if (!valid) np = npo;
+        if (rr) {
+          any = true;
+          if (hl == 0) {
+            sm.nrm[q0 + c] = nq;
+            sm.dsc[q0 + c] = dq;
+            sm.chg[p0 + hw] |= 2;
+            sm.chg[q0 + c] |= 2;
+          }
+        }
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (hl == 0) *(volatile int*)&sm.qcnt[c] = r + 1;
+    }
+    __syncthreads();
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
+  }
+
+  __device__ void fold_and_norms(Smem& sm, double tol, bool first) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < Nw; c += NWARP) {
+      const double d = first ? 1.0 : sm.dsc[c];
+      double2* p = W + (size_t)c * Mw;
+      double acc = 0.0;
+      for (int y = lane; y < Mw; y += 32) {
+        double2 v = p[y];
+        if (d != 1.0) {
+          v = cscale(v, d);
+          p[y] = v;
+        }
+        acc += abs2(v);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) sm.nrm[c] = acc;
+    }
+    __syncthreads();  // every column folded before the scales are reset
+    for (int c = threadIdx.x; c < Nw; c += NT) {
+      sm.dsc[c] = 1.0;
+      sm.chg[c] = first ? 1 : ((sm.chg[c] >> 1) & 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int c = 0; c < Nw; ++c) t += sm.nrm[c];
+      sm.scale = t;
+      sm.flag = 0;
+      sm.offmax = 0.0;
+    }
+    __syncthreads();
+    tol2 = tol * tol;
+    const double dead = 1e-28 * sm.scale;
+    for (int c = warp; c < Nw; c += NWARP) {
+      const double v = sm.nrm[c];
+      if (v < dead && v > 0.0) {
+        double2* p = W + (size_t)c * Mw;
+        for (int y = lane; y < Mw; y += 32) p[y] = cz();
+        if (lane == 0) sm.nrm[c] = 0.0;
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ void sweep(Smem& sm) {
+    offmax = 0.0;
+    const int hw = threadIdx.x >> 4;
+    for (int bp = 0; bp < nblk; ++bp) {
+      stage(bp);
+      within(bp, sm);
+      HCol<HR> pc;
+      double np = 0.0, dp = 1.0;
+      const bool more = bp + 1 < nblk;
+      if (more) {  // P straight from the staged block
+        const uint32_t l = lrow();
+#pragma unroll
+        for (int q = 0; q < HR; ++q) pc.v[q] = lds2(scol(hw) + l + 256u * q);
+        if (hw < ncl[bp]) {
+          np = sm.nrm[start[bp] + hw];
+          dp = sm.dsc[start[bp] + hw];
+        }
+      }
+      __syncthreads();
+      unstage(bp);
+      if (!more) break;
+      for (int bq = bp + 1; bq < nblk; ++bq) {
+        stage(bq);
+        cross(pc, np, dp, bp, bq, sm);
+        unstage(bq);
+      }
+      if (hw < ncl[bp]) {
+        double2* p = W + (size_t)(start[bp] + hw) * Mw;
+        const int l = threadIdx.x & 15;
+#pragma unroll
+        for (int q = 0; q < HR; ++q) {
+          const int y = l + 16 * q;
+          if (y < Mw) p[y] = pc.v[q];
+        }
+        if ((threadIdx.x & 15) == 0) {
+          sm.nrm[start[bp] + hw] = np;
+          sm.dsc[start[bp] + hw] = dp;
+        }
+      }
+      __syncthreads();
+    }
+    if ((threadIdx.x & 15) == 0 && offmax > 0.0) atomic_max_pos(&sm.offmax, offmax);
+  }
+};
+
+__device__ int jacobi_wide(double2* W, int Mw, int Nw, Smem& sm, double2* smem) {
+  JacobiW J;
+  J.W = W;
+  J.Mw = Mw;
+  J.Nw = Nw;
+  J.nblk = (Nw + JB - 1) / JB;
+  J.base = (uint32_t)__cvta_generic_to_shared(smem);
+  J.start[0] = 0;
+  for (int b = 0; b < 8; ++b) {
+    J.ncl[b] = (b < J.nblk) ? (Nw / J.nblk + (b >= J.nblk - Nw % J.nblk ? 1 : 0)) : 0;
+    J.start[b + 1] = J.start[b] + J.ncl[b];
+  }
+  const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16 * TB_TOLSCALE;
+  __syncthreads();
+  int sweep = 0;
+  bool conv = false;
+  for (; sweep < MAXSWEEP; ++sweep) {
+    J.fold_and_norms(sm, tol, sweep == 0);
+    J.sweep(sm);
+    __syncthreads();
+    if (sm.flag == 0 || sm.offmax < 1e-16 * TB_TOLSCALE) {
+      conv = true;
+      break;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sm.sweeps = sweep + 1;
+  // fold the final scales
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < Nw; c += NWARP) {
+      const double d = sm.dsc[c];
+      if (d == 1.0) continue;
+      double2* p = W + (size_t)c * Mw;
+      for (int y = lane; y < Mw; y += 32) p[y] = cscale(p[y], d);
+    }
+  }
+  __syncthreads();
+  return conv ? Nw : -Nw;
+}
+
 // dispatcher: returns the number of (possibly padded) result columns in W;
 // sets status bit 0 on non-convergence
 __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
@@ -905,6 +1226,7 @@ __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* 
   else if (Mw <= 32 && Nw <= 128) neff = jacobi_half<2>(W, Mw, Nw, sm, smem);
   else if (Mw <= 64 && Nw <= 128) neff = jacobi_half<4>(W, Mw, Nw, sm, smem);
   else if (Mw <= 128 && Nw <= 128) neff = jacobi_half<8>(W, Mw, Nw, sm, smem);
+  else if (Mw <= 256 && Nw <= 256) neff = jacobi_wide(W, Mw, Nw, sm, smem);
   else {
     const int sw = hestenes(W, Mw, Nw, sm);
     neff = (sw > MAXSWEEP) ? -Nw : Nw;
@@ -1149,7 +1471,168 @@ __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm
 
 // Y = W^H is in W (ld = Nw); returns Neff, W = rotated columns of L (ld = Mw),
 // rows in pivoted order (sm.qpinv maps an original row to its position)
+// Column-pivoted MGS QR for the wide problems (Y: Nw <= 256 rows x Mw <= 256
+// columns, col-major, ld = Nw, in global memory).  Same algorithm and outputs
+// as qrcp_mgs (R row-major by original column, sm.qperm / sm.qpinv, returns
+// the numerical rank), but the columns stay in global memory (L2): half-warp
+// k owns columns k, k+32, ..., a column is 16 lanes x 16 rows in registers
+// while it is updated, and q is streamed from shared memory.
+__device__ int qrcp_wide(double2* Y, int Nw, int Mw, double2* R, Smem& sm, double2* smem) {
+  constexpr int HR = 16;
+  const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15, lane = threadIdx.x & 31;
+  const uint32_t qaddr = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t l = hl * 16u;
+  const int nown = (Mw - hw + 31) / 32;  // columns owned by this half
+  for (int k = 0; k < 8; ++k) {
+    const int c = hw + 32 * k;
+    double acc = 0.0;
+    if (k < nown) {
+      HCol<HR> v;
+      hcol_ldg(v, Y + (size_t)c * Nw, Nw);
+#pragma unroll
+      for (int q = 0; q < HR; ++q) acc += abs2(v.v[q]);
+    }
+    acc = half_sum(acc);
+    if (hl == 0 && k < nown) sm.nrm[c] = sm.nref[c] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int c = 0; c < Mw; ++c) t += sm.nrm[c];
+    sm.scale = 1e-28 * t;
+  }
+  auto local_best = [&]() {  // lanes 0-7 of a half hold its candidates
+    const int c = hw + 32 * (hl & 7);
+    const bool ok = hl < 8 && (hl & 7) < nown;
+    double best = ok ? sm.nrm[c] : -1.0;
+    int bi = ok ? c : -1;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
+    }
+    if (hl == 0) {
+      sm.wbest[hw] = best;
+      sm.wbidx[hw] = bi;
+    }
+  };
+  local_best();
+  __syncthreads();
+  const double dead = sm.scale;
+  const int rmax = min(Mw, Nw);
+  int j = 0;
+  for (; j < rmax; ++j) {
+    // global pivot: same packed-key redux as qrcp_mgs (8 index bits here)
+    const int wi = sm.wbidx[lane];
+    const double wv = sm.wbest[lane];
+    const unsigned key =
+        (wi >= 0 && wv > dead) ? ((unsigned)__double2hiint(wv) & 0xFFFFFF00u) | (unsigned)(255 - wi) : 0u;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+    if (kmax == 0u) break;
+    const int p = 255 - (int)(kmax & 255u);
+    const int owner = p & 31;
+    if ((owner >> 1) == (threadIdx.x >> 5)) {
+      const bool me = hw == owner;
+      HCol<HR> v;
+      hcol_ldg(v, Y + (size_t)p * Nw, Nw);
+      double nn = 0.0;
+#pragma unroll
+      for (int q = 0; q < HR; ++q) nn += abs2(v.v[q]);
+      nn = half_sum(nn);
+      const double rn = sqrt(nn), inv = 1.0 / rn;
+      if (me) {
+#pragma unroll
+        for (int q = 0; q < HR; ++q) sts2(qaddr + l + 256u * q, cscale(v.v[q], inv));
+        if (hl == 0) {
+          R[(size_t)j * Mw + p] = make_double2(rn, 0.0);
+          sm.qperm[j] = p;
+          sm.nrm[p] = -1.0;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 0; k < 8; ++k) {
+      const int c = hw + 32 * k;
+      const bool valid = k < nown && sm.nrm[c] >= 0.0;
+      if (!__any_sync(0xffffffffu, valid)) continue;
+      HCol<HR> y;
+      if (valid) hcol_ldg(y, Y + (size_t)c * Nw, Nw);
+      else {
+#pragma unroll
+        for (int q = 0; q < HR; ++q) y.v[q] = cz();
+      }
+      double2 d = cz(), e = cz();
+#pragma unroll
+      for (int q = 0; q < HR; q += 2) {
+        cfmac(d, lds2(qaddr + l + 256u * q), y.v[q]);
+        cfmac(e, lds2(qaddr + l + 256u * (q + 1)), y.v[q + 1]);
+      }
+      d.x = half_sum(d.x + e.x);
+      d.y = half_sum(d.y + e.y);
+      if (!valid) d = cz();
+#pragma unroll
+      for (int q = 0; q < HR; ++q) {
+        const double2 qq = lds2(qaddr + l + 256u * q);
+        y.v[q].x -= d.x * qq.x - d.y * qq.y;
+        y.v[q].y -= d.x * qq.y + d.y * qq.x;
+      }
+      double nr = valid ? sm.nrm[c] - abs2(d) : 0.0;
+      const bool f = valid && nr < 1e-2 * sm.nref[c];
+      if (__any_sync(0xffffffffu, f)) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < HR; ++q) acc += abs2(y.v[q]);
+        acc = half_sum(acc);
+        if (f) nr = acc;
+      }
+      if (valid) {
+        hcol_stg(Y + (size_t)c * Nw, y, Nw);
+        if (hl == 0) {
+          sm.nrm[c] = nr;
+          if (f) sm.nref[c] = nr;
+          R[(size_t)j * Mw + c] = d;
+        }
+      }
+    }
+    __syncwarp();
+    local_best();
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
+  if (threadIdx.x == 0) {
+    int k = j;
+    for (int c = 0; c < Mw; ++c)
+      if (sm.nrm[c] >= 0.0) sm.qperm[k++] = c;
+    for (int k2 = 0; k2 < Mw; ++k2) sm.qpinv[sm.qperm[k2]] = k2;
+  }
+  __syncthreads();
+  return j;
+}
+
+__device__ int precond_jacobi_wide(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
+  const long long t0 = prof_clock();
+  const int r = qrcp_wide(W, Nw, Mw, X, sm, smem);
+  if (threadIdx.x == 0 && sm.prof) {
+    atomicAdd(&sm.prof[12], (unsigned long long)(prof_clock() - t0));
+    atomicAdd(&sm.prof[8], 1ull);
+  }
+  const int K = min(Mw, Nw);
+  int neff = 0;
+  if (r > 0) {
+    build_l(X, Mw, r, W, sm);
+    neff = jacobi(W, Mw, r, sm, smem, status);
+  }
+  if (neff < K) {
+    for (int e = threadIdx.x; e < (K - neff) * Mw; e += NT) W[(size_t)neff * Mw + e] = cz();
+    __syncthreads();
+  }
+  return max(neff, K);
+}
+
 __device__ int precond_jacobi(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
+  if (Nw > 128 || Mw > 128) return precond_jacobi_wide(W, X, Mw, Nw, sm, smem, status);
   if (Nw <= 16) return precond_jacobi_t<1>(W, X, Mw, Nw, sm, smem, status);
   if (Nw <= 32) return precond_jacobi_t<2>(W, X, Mw, Nw, sm, smem, status);
   if (Nw <= 64) return precond_jacobi_t<4>(W, X, Mw, Nw, sm, smem, status);
@@ -1196,7 +1679,7 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
 
   // QR-preconditioned path for sizeable problems: W holds Y = W_jac^H, i.e.
   // theta is written in the opposite orientation (see precond_jacobi)
-  const bool pre = jb.precond && Mw >= 32 && Nw >= 32 && Mw <= 128 && Nw <= 128;
+  const bool pre = jb.precond && Mw >= 32 && Nw >= 32;
   const bool orient = pre ? !merge_right : merge_right;  // true: col-major theta
   const int ldw = orient ? M : N;
 
@@ -1862,7 +2345,7 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
   double2* W0 = W0g + mat_stride * b;
   double2* X = Xg + mat_stride * b;
   const double2* A = a + (size_t)b * m * n;
-  const bool pre = precond && m >= 32 && n >= 32 && m <= 128 && n <= 128;
+  const bool pre = precond && m >= 32 && n >= 32;
   // left singular vectors of A (m x n): columns of W = A, or Y = A^H when preconditioned
   for (int e = threadIdx.x; e < m * n; e += NT) {
     const int y = e / n, c = e - y * n;

@@ -33,6 +33,19 @@ def _svd_gpu(engine, a):
 
 @pytest.mark.parametrize("m,n", [(2, 2), (4, 16), (16, 4), (32, 32), (64, 128), (128, 64), (128, 128), (256, 256)])
 def test_jacobi_svd_matches_lapack(engine, m, n):
+    _check_svd(engine, m, n)
+
+
+# chi = 128 shapes (the wide path: block-streamed Jacobi + global-memory QRCP),
+# including ragged column blocks, with and without the QR preconditioner
+@pytest.mark.parametrize("m,n", [(256, 33), (129, 129), (200, 97), (97, 200), (256, 128), (136, 256)])
+@pytest.mark.parametrize("precond", ["0", "1"])
+def test_wide_svd_matches_lapack(engine, monkeypatch, m, n, precond):
+    monkeypatch.setenv("TB_PRECOND", precond)
+    _check_svd(engine, m, n)
+
+
+def _check_svd(engine, m, n):
     rng = np.random.default_rng(m * 1000 + n)
     k = min(m, n)
     # graded spectrum down to 1e-14 plus an exactly rank-deficient tail

@@ -366,6 +366,15 @@ __device__ __forceinline__ void sts2(uint32_t a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {  // shared, CTA scope
+  int v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
 // Rotation of one pair.  Identity when s == 0 (c = 1, e = 1).
 struct Rot {
   double c, s, er, ei, tg, t;
@@ -654,11 +663,10 @@ struct JacobiH {
       for (int x = 0; x < S; ++x) {
         const int sq = x == 0 ? sq0 : (x == 1 ? sq1 : sq2);
         int* cnt = &sm.qcnt[x * 32 + c];
-        if (m > 0) {
+        if (m > 0) {  // acquire the previous visit's column (lane 0), then share it via the warp barrier
           if (hl == 0)
-            while (*(volatile int*)cnt < m) {}
+            while (ld_acquire(cnt) < m) {}
           __syncwarp();
-          __threadfence_block();
         }
         const bool valid = vp && c < sm.jncol[sq] && ((sm.chg[sp * JB + hw] | sm.chg[sq * JB + c]) & 1);
         if (__any_sync(0xffffffffu, valid)) {
@@ -679,9 +687,8 @@ struct JacobiH {
             }
           }
         }
-        __threadfence_block();
-        __syncwarp();
-        if (hl == 0) *(volatile int*)cnt = m + 1;
+        __syncwarp();  // the half's column stores are ordered before lane 0's release
+        if (hl == 0) st_release(cnt, m + 1);
       }
     }
     __syncthreads();
@@ -1059,9 +1066,8 @@ struct JacobiW {
       const int c = (hw + r) & 31;
       if (r > 0) {
         if (hl == 0)
-          while (*(volatile int*)&sm.qcnt[c] < r) {}
+          while (ld_acquire(&sm.qcnt[c]) < r) {}
         __syncwarp();
-        __threadfence_block();
       }
       const bool valid = vp && c < nQ && ((sm.chg[p0 + hw] | sm.chg[q0 + c]) & 1);
       if (__any_sync(0xffffffffu, valid)) {
@@ -1079,9 +1085,8 @@ struct JacobiW {
           }
         }
       }
-      __threadfence_block();
       __syncwarp();
-      if (hl == 0) *(volatile int*)&sm.qcnt[c] = r + 1;
+      if (hl == 0) st_release(&sm.qcnt[c], r + 1);
     }
     __syncthreads();
     if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;

@@ -737,31 +737,51 @@ struct JacobiH {
     __syncthreads();
   }
 
+  // fold the scales into the columns and take exact norms in one pass
   __device__ void refresh_norms(Smem& sm, double tol, bool first) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    fold_scales(sm, first);
     for (int c = warp; c < JB * nblk; c += NWARP) {
       const int s = c / JB, k = c - s * JB;
+      const double d = first ? 1.0 : sm.dsc[c];
       double acc = 0.0;
       if (s < 3) {
-        const double2* p = (const double2*)nullptr;
-        (void)p;
-        for (int y = lane; y < LD; y += 32) acc += abs2(lds2(scol(s, k) + 16u * y));
+        for (int y = lane; y < LD; y += 32) {
+          const uint32_t a = scol(s, k) + 16u * y;
+          double2 v = lds2(a);
+          if (d != 1.0) {
+            v = cscale(v, d);
+            sts2(a, v);
+          }
+          acc += abs2(v);
+        }
       } else {
-        const double2* p = G + (size_t)k * Mw;
-        for (int y = lane; y < Mw; y += 32) acc += abs2(p[y]);
+        double2* p = G + (size_t)k * Mw;
+        for (int y = lane; y < Mw; y += 32) {
+          double2 v = p[y];
+          if (d != 1.0) {
+            v = cscale(v, d);
+            p[y] = v;
+          }
+          acc += abs2(v);
+        }
       }
       acc = warp_sum(acc);
       if (lane == 0) sm.nrm[c] = acc;
     }
-    for (int c = threadIdx.x; c < JB * nblk; c += NT) sm.chg[c] = first ? 1 : ((sm.chg[c] >> 1) & 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    __syncthreads();  // every column folded before the scales are reset
+    for (int c = threadIdx.x; c < JB * nblk; c += NT) {
+      sm.dsc[c] = 1.0;
+      sm.chg[c] = first ? 1 : ((sm.chg[c] >> 1) & 1);
+    }
+    if (threadIdx.x < 32) {
       double t = 0.0;
-      for (int c = 0; c < JB * nblk; ++c) t += sm.nrm[c];
-      sm.scale = t;
-      sm.flag = 0;
-      sm.offmax = 0.0;
+      for (int c = threadIdx.x; c < JB * nblk; c += 32) t += sm.nrm[c];
+      t = warp_sum(t);
+      if (threadIdx.x == 0) {
+        sm.scale = t;
+        sm.flag = 0;
+        sm.offmax = 0.0;
+      }
     }
     __syncthreads();
     tol2 = tol * tol;
@@ -794,6 +814,7 @@ struct JacobiH {
       load_p(pc, np, dp, 3, sm);
       cross(pc, np, dp, sm.jncol[3], 3, 0, 1, 2, 3, sm);
       // swap contents of A and G (P holds the current G columns)
+      const long long tsw = prof_clock();
       {
         HCol<HR> t;
         double nt, dt;
@@ -815,6 +836,7 @@ struct JacobiH {
         }
         __syncthreads();
       }
+      if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[27], (unsigned long long)(prof_clock() - tsw));
       within(0, 0, 0, 1, sm);
       load_p(pc, np, dp, 3, sm);
       cross(pc, np, dp, sm.jncol[3], 3, 1, 2, 2, 2, sm);
@@ -844,6 +866,7 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   J.nblk = (Nw + JB - 1) / JB;
   J.base = (uint32_t)__cvta_generic_to_shared(smem);
   J.G = W + (size_t)3 * JB * Mw;
+  const long long tj0 = prof_clock();
   int start[5];
   start[0] = 0;
   int ncl[4];
@@ -875,11 +898,13 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     smem[e] = (k < ncl[sb] && y < Mw) ? W[(size_t)(start[sb] + k) * Mw + y] : cz();
   }
   __syncthreads();
+  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[25], (unsigned long long)(prof_clock() - tj0));
   int sweep = 0;
   bool conv = false;
   for (; sweep < MAXSWEEP; ++sweep) {
     const long long ts0 = prof_clock();
     J.refresh_norms(sm, tol, sweep == 0);
+    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[26], (unsigned long long)(prof_clock() - ts0));
     J.sweep(sm);
     __syncthreads();
     if (threadIdx.x == 0 && sm.prof && Mw == 128 && sweep < 16) {
@@ -893,12 +918,14 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     __syncthreads();
   }
   if (threadIdx.x == 0) sm.sweeps = sweep + 1;
+  const long long tw0 = prof_clock();
   J.fold_scales(sm, false);
   for (int e = threadIdx.x; e < nsm * JB * Mw; e += NT) {
     const int c = e / Mw, y = e - c * Mw;
     W[(size_t)c * Mw + y] = smem[(size_t)c * LD + y];
   }
   __syncthreads();
+  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[28], (unsigned long long)(prof_clock() - tw0));
   const int neff = (J.nblk == 1) ? Nw : JB * J.nblk;
   return conv ? neff : -neff;
 }
@@ -1296,10 +1323,11 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     if (hl == 0 && cg < Mw) sm.nrm[cg] = sm.nref[cg] = acc;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     double t = 0.0;
-    for (int c = 0; c < Mw; ++c) t += sm.nrm[c];
-    sm.scale = 1e-28 * t;  // dead threshold on residual norm^2
+    for (int c = threadIdx.x; c < Mw; c += 32) t += sm.nrm[c];
+    t = warp_sum(t);
+    if (threadIdx.x == 0) sm.scale = 1e-28 * t;  // dead threshold on residual norm^2
   }
   // per-half pivot candidate over the owned columns (lanes 0-3 of the half)
   auto local_best = [&]() {
@@ -1463,7 +1491,9 @@ __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm
   const int K = min(Mw, Nw);
   int neff = 0;
   if (r > 0) {
+    const long long tb0 = prof_clock();
     build_l(X, Mw, r, W, sm);
+    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[24], (unsigned long long)(prof_clock() - tb0));
     neff = jacobi(W, Mw, r, sm, smem, status);
   }
   // the numerically dead directions are exact zero columns
@@ -1770,7 +1800,9 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
     prof_add(jb, 10, 1);
     prof_add(jb, 11, sm.sweeps);
   }
+  const long long tss = prof_clock();
   sort_sigma(W, Mw, Neff, sm);
+  prof_add(jb, 29, prof_clock() - tss);
 
   // truncation rule + renormalisation (_kernel.py:118-131)
   if (threadIdx.x == 0) {

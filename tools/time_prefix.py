@@ -34,3 +34,4 @@ print("phase share: jacobi %.3f (qrcp %.3f) qr %.3f gemm+gate %.3f post %.3f mea
 print("qrcp calls %d avg steps %.1f cyc/step %.0f | within %.3f cross %.3f of total" % (
     pr[8], pr[15]/max(pr[8],1), pr[12]/max(pr[15],1), pr[13]/tot, pr[14]/tot))
 print("Mw=128 cycles per sweep index (k cycles):", [int(pr[40+k]/max(pr[56+min(k,7)],1)/1e3) for k in range(8)], "counts", pr[56:64].astype(int).tolist())
+print("jacobi overheads (share of total): build_l %.3f staging %.3f refresh %.3f swap %.3f writeback %.3f sort_sigma %.3f" % tuple(pr[24:30] / tot))

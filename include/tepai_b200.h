@@ -15,6 +15,8 @@
  *                        (mps.py:276-288) + expectation of Z_j + signed sums
  *   tb_svd            <- the np.linalg.svd(mat, False) call inside
  *                        _split_theta (_kernel.py:117), exposed for unit tests
+ *   tb_svd_trunc      <- the same call as consumed by the truncation rule
+ *                        (_kernel.py:117-131): only the kept triplets exact
  *
  * Return codes: 0 ok, negative on error; tb_last_error() gives the message.
  */
@@ -78,6 +80,14 @@ int tb_expectation(tb_ctx* ctx, const double* buf, int64_t n, int64_t cap, const
  * vh: [batch][k][n] with k = min(m, n).  Any of u / vh may be NULL. */
 int tb_svd(tb_ctx* ctx, const double* a, int64_t batch, int64_t m, int64_t n, double* s, double* u,
            double* vh);
+
+/* Truncated variant: only the kcut largest triplets are needed (the split
+ * keeps k <= min(chi_cut, K), _kernel.py:118-131).  s[:kcut], u[:, :kcut] and
+ * vh[:kcut] are those of the full SVD, and sum(s^2) is still |a|_F^2; the
+ * tail entries are an orthogonal complement that need not be diagonal.
+ * kcut <= 0 or >= min(m, n) is the full SVD. */
+int tb_svd_trunc(tb_ctx* ctx, const double* a, int64_t batch, int64_t m, int64_t n, int64_t kcut, double* s,
+                 double* u, double* vh);
 
 typedef struct tb_ensemble_desc {
   int32_t n;           /* sites */

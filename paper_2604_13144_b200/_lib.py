@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("TB_LIB") or os.path.join(os.path.dirname(os.path.absp
 
 EXPORTED = (
     "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_debug_profile", "tb_run_stream",
-    "tb_expectation", "tb_svd", "tb_run_ensemble", "tb_run_ensemble_device", "tb_step", "tb_step_device",
+    "tb_expectation", "tb_svd", "tb_svd_trunc", "tb_run_ensemble", "tb_run_ensemble_device", "tb_step", "tb_step_device",
 )
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -74,6 +74,7 @@ def load() -> ctypes.CDLL:
         lib.tb_run_stream.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp, vp, vp, i64, i64, dbl, vp, vp]
         lib.tb_expectation.argtypes = [vp, vp, i64, i64, vp, vp, vp]
         lib.tb_svd.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp]
+        lib.tb_svd_trunc.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp]
         lib.tb_run_ensemble.argtypes = [vp, ctypes.POINTER(EnsembleDesc), ctypes.POINTER(EnsembleOut)]
         lib.tb_run_ensemble_device.argtypes = [vp, ctypes.POINTER(EnsembleDesc), ctypes.POINTER(EnsembleOut), vp]
         lib.tb_step.argtypes = [vp, ctypes.POINTER(StepDesc), ctypes.POINTER(EnsembleOut), i64]

@@ -77,6 +77,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 struct Job {
   int n, cap, chi_cut, pi_local;
   int precond;  // QR-preconditioned Jacobi for problems >= 32 x 32
+  int tail_skip;  // skip pairs of discarded-tail columns (see mark_tail)
   double floor;
   int n_samples, n_ckpt, n_obs;
   const uint32_t* gates;
@@ -121,7 +122,7 @@ struct Smem {
   double dsc[MAXDIM];        // Jacobi column scales (true column = dsc * stored)
   double wbest[32];          // per-half-warp pivot candidates (QRCP)
   int qcnt[3 * 32];          // cross-phase Q visit counters (per slot, column)
-  unsigned char chg[MAXDIM]; // bit0: rotated in the previous sweep, bit1: in this sweep
+  unsigned char chg[MAXDIM]; // bit0: rotated in the previous sweep, bit1: in this sweep, bit2: tail column
   int jncol[4];              // live columns per Jacobi block slot
   int wbidx[32];
   double nref[MAXDIM];
@@ -139,6 +140,8 @@ struct Smem {
   int flag;
   int sweeps;
   int rotcount;
+  int kcut;                  // singular triplets the caller keeps (min(chi_cut, K)); tail pairs beyond are skipped
+  int ntail;                 // columns currently marked as tail (chg bit 2)
   unsigned long long* prof;
   int sample;
   int center;
@@ -520,6 +523,91 @@ __device__ __forceinline__ double half_sum(double v) {
   return v;
 }
 
+constexpr double kTailTol2 = 1e-8;  // (relative coupling 1e-4)^2 for pairs of two tail columns
+
+// ----------------------------------------------------------------------------
+// Tail skipping for truncated splits.  The caller keeps only the kcut largest
+// singular triplets (k <= min(chi_cut, K), _kernel.py:118-131).  Let T be a
+// set of small columns whose total weight sum_T |a|^2 is below half of the
+// kcut-th largest |a|^2.  Once every pair with at least one column outside T
+// has converged, the columns outside T are exact singular vectors, the T block
+// is orthogonal to them, and the largest singular value of the T block (at
+// most its Frobenius norm) lies below the kcut-th singular value.  The kept
+// triplets, the count k and the discarded weight (total - kept, total = the
+// Frobenius norm) are therefore those of the full SVD, and T-T pairs need no
+// exact orthogonality.  They are still rotated down to a relative coupling of
+// 1e-4 (kTailTol2): leaving them fully coupled turns the convergence of the
+// kept-tail pairs linear (each kept column would chase a non-orthogonal tail
+// basis), while the last orders of magnitude — the late-sweep tail work — are
+// skipped.  T is fixed after the first sweep (chg bit 2) and re-checked with
+// the converged norms; a failed check clears T and the sweeps go on.
+// ----------------------------------------------------------------------------
+template <class Live>
+__device__ __forceinline__ void tail_rank(const Smem& sm, int ncol, Live live, int c, double a, int& rank,
+                                          double& suffix) {
+  rank = 0;
+  suffix = 0.0;
+  for (int j = 0; j < ncol; ++j) {
+    if (!live(j)) continue;
+    const double b = sm.nrm[j];
+    const bool before = b > a || (b == a && j < c);
+    rank += before ? 1 : 0;
+    suffix += before ? 0.0 : b;
+  }
+}
+
+// mark T (chg bit 2); returns |T| (CTA-uniform)
+template <class Live>
+__device__ int mark_tail(Smem& sm, int ncol, Live live) {
+  const int c = threadIdx.x;
+  const bool me = c < ncol && live(c);
+  const int nlive = __syncthreads_count(me);
+  if (nlive <= sm.kcut) return 0;
+  const double a = me ? sm.nrm[c] : 0.0;
+  int rank = 0;
+  double suf = 0.0;
+  if (me) {
+    tail_rank(sm, ncol, live, c, a, rank, suf);
+    if (rank == sm.kcut - 1) sm.invsig_tmp = 0.5 * a;
+  }
+  __syncthreads();
+  const bool t = me && rank >= sm.kcut && suf < sm.invsig_tmp;
+  if (c < ncol) sm.chg[c] = t ? (sm.chg[c] | 4) : (sm.chg[c] & ~4);
+  const int nt = __syncthreads_count(t);
+  if (threadIdx.x == 0) sm.ntail = nt;
+  return nt;
+}
+
+// true when the converged norms still certify T (see above); otherwise T is
+// cleared and every column is flagged as changed so that all pairs are swept
+template <class Live>
+__device__ bool tail_ok(Smem& sm, int ncol, Live live) {
+  const int c = threadIdx.x;
+  const bool me = c < ncol && live(c);
+  if (me) {
+    int rank;
+    double suf;
+    tail_rank(sm, ncol, live, c, sm.nrm[c], rank, suf);
+    if (rank == sm.kcut - 1) sm.invsig_tmp = 0.5 * sm.nrm[c];
+  }
+  const bool t = me && (sm.chg[c] & 4);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double st = 0.0;
+    for (int j = threadIdx.x; j < ncol; j += 32)
+      if (live(j) && (sm.chg[j] & 4)) st += sm.nrm[j];
+    st = warp_sum(st);
+    if (threadIdx.x == 0) sm.red[0] = (st < sm.invsig_tmp) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const bool ok = sm.red[0] != 0.0;
+  (void)t;
+  if (!ok && c < ncol) sm.chg[c] = (sm.chg[c] & ~4) | 2;
+  __syncthreads();
+  if (!ok && threadIdx.x == 0) sm.ntail = 0;
+  return ok;
+}
+
 // one pair per half-warp; `valid` may differ between the halves.  na / nb are
 // the TRUE squared norms, da / db the column scales; sa / sb the shared-memory
 // homes of the two columns (written only when THIS half rotates).  Returns
@@ -606,14 +694,16 @@ struct JacobiH {
     for (int k = 0; k < nsteps; ++k) {
       const int m = per * k + (hw >> 4), p = hw & 15;
       const int r = m / ns, x = m - r * ns;
-      bool valid = false;
+      bool valid = false, tt = false;
       int s = 0, i = 0, j = 0;
       if ((hw >> 4) < per && r < rounds) {
         s = (x == 0) ? s0 : (x == 1 ? s1 : s2);
         const int nb = sm.jncol[s], nbp = nb + (nb & 1);
         if (r < nbp - 1 && p < nbp / 2) {
           rr_pair(r, p, nbp, i, j);
-          valid = i < nb && j < nb && ((sm.chg[s * JB + i] | sm.chg[s * JB + j]) & 1);
+          const unsigned ci = sm.chg[s * JB + i], cj = sm.chg[s * JB + j];
+          valid = i < nb && j < nb && ((ci | cj) & 1);
+          tt = (ci & cj & 4) != 0;
         }
       }
       if (__any_sync(0xffffffffu, valid)) {
@@ -625,7 +715,7 @@ struct JacobiH {
         hcol_lds(b, aj);
         double na = valid ? sm.nrm[s * JB + i] : 0.0, nb2 = valid ? sm.nrm[s * JB + j] : 0.0;
         double da = sm.dsc[s * JB + i], db = sm.dsc[s * JB + j];
-        const bool rr = rot_half<HR, false>(a, b, ai, aj, na, nb2, da, db, valid, tol2, offmax);
+        const bool rr = rot_half<HR, false>(a, b, ai, aj, na, nb2, da, db, valid, tt ? kTailTol2 : tol2, offmax);
         if (rr) {
           any = true;
           if (hl == 0) {
@@ -668,14 +758,16 @@ struct JacobiH {
             while (ld_acquire(cnt) < m) {}
           __syncwarp();
         }
-        const bool valid = vp && c < sm.jncol[sq] && ((sm.chg[sp * JB + hw] | sm.chg[sq * JB + c]) & 1);
+        const unsigned cp = sm.chg[sp * JB + hw], cq = sm.chg[sq * JB + c];
+        const bool valid = vp && c < sm.jncol[sq] && ((cp | cq) & 1);
+        const double tl2 = (cp & cq & 4) ? kTailTol2 : tol2;
         if (__any_sync(0xffffffffu, valid)) {
           HCol<HR> q;
           const uint32_t aq = scol(sq, c);
           hcol_lds(q, aq);  // unconditional (see within)
           double nq = valid ? sm.nrm[sq * JB + c] : 0.0, dq = sm.dsc[sq * JB + c];
           const double npo = np;
-          const bool rr = rot_half<HR, true>(pc, q, 0u, aq, np, nq, dp, dq, valid, tol2, offmax);
+          const bool rr = rot_half<HR, true>(pc, q, 0u, aq, np, nq, dp, dq, valid, tl2, offmax);
           if (!valid) np = npo;
           if (rr) {
             any = true;
@@ -771,7 +863,7 @@ struct JacobiH {
     __syncthreads();  // every column folded before the scales are reset
     for (int c = threadIdx.x; c < JB * nblk; c += NT) {
       sm.dsc[c] = 1.0;
-      sm.chg[c] = first ? 1 : ((sm.chg[c] >> 1) & 1);
+      sm.chg[c] = first ? 1 : (((sm.chg[c] >> 1) & 1) | (sm.chg[c] & 4));
     }
     if (threadIdx.x < 32) {
       double t = 0.0;
@@ -899,11 +991,14 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   }
   __syncthreads();
   if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[25], (unsigned long long)(prof_clock() - tj0));
+  auto live = [&](int c) { return (c & (JB - 1)) < sm.jncol[c / JB]; };
+  if (threadIdx.x == 0) sm.ntail = 0;
   int sweep = 0;
   bool conv = false;
   for (; sweep < MAXSWEEP; ++sweep) {
     const long long ts0 = prof_clock();
     J.refresh_norms(sm, tol, sweep == 0);
+    if (sweep == 1) mark_tail(sm, JB * J.nblk, live);
     if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[26], (unsigned long long)(prof_clock() - ts0));
     J.sweep(sm);
     __syncthreads();
@@ -912,6 +1007,7 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
       atomicAdd(&sm.prof[56 + min(sweep, 7)], 1ull);
     }
     if (sm.flag == 0 || sm.offmax < 1e-16 * TB_TOLSCALE) {
+      if (sm.ntail > 0 && !tail_ok(sm, JB * J.nblk, live)) continue;
       conv = true;
       break;
     }
@@ -977,7 +1073,7 @@ struct JacobiW {
   // b in smem at sb.  na/nb true squared norms, da/db scales.
   template <bool A_REG>
   __device__ __forceinline__ bool rot(HCol<HR>& a, uint32_t sa, uint32_t sb, double& na, double& nb, double& da,
-                                      double& db, bool valid) {
+                                      double& db, bool valid, double tl2) {
     const uint32_t l = lrow();
     double2 g = cz(), h = cz();
 #pragma unroll
@@ -998,7 +1094,7 @@ struct JacobiW {
     const double dd = da * db;
     gr *= dd;
     gi *= dd;
-    const Rot p = rot_params(gr, gi, na, nb, valid, tol2);
+    const Rot p = rot_params(gr, gi, na, nb, valid, tl2);
     const bool mine = p.s != 0.0;
     if (mine) {
       double r;
@@ -1055,16 +1151,18 @@ struct JacobiW {
     bool any = false;
     for (int r = 0; r < nbp - 1; ++r) {
       int i = 0, j = 0;
-      bool valid = false;
+      bool valid = false, tt = false;
       if (hw < nbp / 2) {
         rr_pair(r, hw, nbp, i, j);
-        valid = i < nb && j < nb && ((sm.chg[c0 + i] | sm.chg[c0 + j]) & 1);
+        const unsigned ci = sm.chg[c0 + i], cj = sm.chg[c0 + j];
+        valid = i < nb && j < nb && ((ci | cj) & 1);
+        tt = (ci & cj & 4) != 0;
       }
       if (__any_sync(0xffffffffu, valid)) {
         HCol<HR> dummy;
         double na = valid ? sm.nrm[c0 + i] : 0.0, nb2 = valid ? sm.nrm[c0 + j] : 0.0;
         double da = sm.dsc[c0 + i], db = sm.dsc[c0 + j];
-        if (rot<false>(dummy, scol(i), scol(j), na, nb2, da, db, valid)) {
+        if (rot<false>(dummy, scol(i), scol(j), na, nb2, da, db, valid, tt ? kTailTol2 : tol2)) {
           any = true;
           if (hl == 0) {
             sm.nrm[c0 + i] = na;
@@ -1096,11 +1194,13 @@ struct JacobiW {
           while (ld_acquire(&sm.qcnt[c]) < r) {}
         __syncwarp();
       }
-      const bool valid = vp && c < nQ && ((sm.chg[p0 + hw] | sm.chg[q0 + c]) & 1);
+      const unsigned cp = sm.chg[p0 + hw], cq = sm.chg[q0 + c];
+      const bool valid = vp && c < nQ && ((cp | cq) & 1);
+      const double tl2 = (cp & cq & 4) ? kTailTol2 : tol2;
       if (__any_sync(0xffffffffu, valid)) {
         double nq = valid ? sm.nrm[q0 + c] : 0.0, dq = c < nQ ? sm.dsc[q0 + c] : 1.0;
         const double npo = np;
-        const bool rr = rot<true>(pc, 0u, scol(c), np, nq, dp, dq, valid);
+        const bool rr = rot<true>(pc, 0u, scol(c), np, nq, dp, dq, valid, tl2);
         if (!valid) np = npo;
         if (rr) {
           any = true;
@@ -1139,7 +1239,7 @@ struct JacobiW {
     __syncthreads();  // every column folded before the scales are reset
     for (int c = threadIdx.x; c < Nw; c += NT) {
       sm.dsc[c] = 1.0;
-      sm.chg[c] = first ? 1 : ((sm.chg[c] >> 1) & 1);
+      sm.chg[c] = first ? 1 : (((sm.chg[c] >> 1) & 1) | (sm.chg[c] & 4));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1221,14 +1321,18 @@ __device__ int jacobi_wide(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     J.start[b + 1] = J.start[b] + J.ncl[b];
   }
   const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16 * TB_TOLSCALE;
+  auto live = [](int) { return true; };
+  if (threadIdx.x == 0) sm.ntail = 0;
   __syncthreads();
   int sweep = 0;
   bool conv = false;
   for (; sweep < MAXSWEEP; ++sweep) {
     J.fold_and_norms(sm, tol, sweep == 0);
+    if (sweep == 1) mark_tail(sm, Nw, live);
     J.sweep(sm);
     __syncthreads();
     if (sm.flag == 0 || sm.offmax < 1e-16 * TB_TOLSCALE) {
+      if (sm.ntail > 0 && !tail_ok(sm, Nw, live)) continue;
       conv = true;
       break;
     }
@@ -1366,33 +1470,39 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     const int p = 127 - (int)(kmax & 127u);
     const long long tt1 = prof_clock();
     tqa += tt1 - tt0;
-    const int owner = (p < 3 * JB) ? (p & 31) : (p - 3 * JB);
-    if ((owner >> 1) == (threadIdx.x >> 5)) {  // whole warp (half_sum shuffles span it)
-      const bool me = hw == owner;
-      HCol<HR> v;
-      if (p < 3 * JB) hcol_lds(v, base + (uint32_t)p * CB);
-      else v = g;
+    // Every half normalises the pivot column itself (bit-identical results),
+    // reading it straight from its shared-memory home; only a register-held
+    // pivot (columns >= 96) is first published through the q buffer, which
+    // costs the one extra barrier.  The owner half never touches column p in
+    // this step, so the reads need no other ordering than the barrier that
+    // closed the previous step.
+    const bool regp = p >= 3 * JB;
+    const int owner = regp ? (p - 3 * JB) : (p & 31);
+    uint32_t src = base + (uint32_t)p * CB;
+    if (regp) {
+      if (hw == owner) hcol_sts(qaddr, g);
+      __syncthreads();
+      src = qaddr;
+    }
+    const long long tt2 = prof_clock();
+    HCol<HR> qv;
+    hcol_lds(qv, src);
+    {
       double nn = 0.0;
 #pragma unroll
-      for (int q = 0; q < HR; ++q) nn += abs2(v.v[q]);
+      for (int q = 0; q < HR; ++q) nn += abs2(qv.v[q]);
       nn = half_sum(nn);
       const double rn = sqrt(nn), inv = 1.0 / rn;
 #pragma unroll
-      for (int q = 0; q < HR; ++q) v.v[q] = cscale(v.v[q], inv);
-      if (me) hcol_sts(qaddr, v);
-      if (me && hl == 0) {
+      for (int q = 0; q < HR; ++q) qv.v[q] = cscale(qv.v[q], inv);
+      if (hw == owner && hl == 0) {
         R[(size_t)j * Mw + p] = make_double2(rn, 0.0);
         sm.qperm[j] = p;
-        sm.nrm[p] = -1.0;
       }
     }
-    const long long tt2 = prof_clock();
-    __syncthreads();
     const long long tt3 = prof_clock();
     tqb += tt2 - tt1;
     tqc += tt3 - tt2;
-    HCol<HR> qv;
-    hcol_lds(qv, qaddr);
     // MGS update of one column per half: r = q^H y, y -= r q
     auto upd = [&](HCol<HR>& y, int c, bool valid) {
       double2 d = cz(), e = cz();
@@ -1427,7 +1537,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
 #pragma unroll 1
     for (int k = 0; k < 3; ++k) {
       const int c = hw + 32 * k;
-      const bool valid = c < nsm && sm.nrm[c] >= 0.0;
+      const bool valid = c < nsm && c != p && sm.nrm[c] >= 0.0;
       if (!__any_sync(0xffffffffu, valid)) continue;
       HCol<HR> y;
       if (valid) hcol_lds(y, base + (uint32_t)c * CB);
@@ -1439,9 +1549,10 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
       if (valid) hcol_sts(base + (uint32_t)c * CB, y);
     }
     {
-      const bool valid = cg < Mw && sm.nrm[cg] >= 0.0;
+      const bool valid = cg < Mw && cg != p && sm.nrm[cg] >= 0.0;
       if (__any_sync(0xffffffffu, valid)) upd(g, cg, valid);
     }
+    if (hw == owner && hl == 0) sm.nrm[p] = -1.0;
     __syncwarp();
     local_best();
     const long long tt4 = prof_clock();
@@ -1452,8 +1563,8 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
   if (threadIdx.x == 0 && sm.prof) {
     atomicAdd(&sm.prof[15], (unsigned long long)j);
     atomicAdd(&sm.prof[32], (unsigned long long)tqa);   // pivot selection
-    atomicAdd(&sm.prof[33], (unsigned long long)tqb);   // owner normalisation (thread 0's view)
-    atomicAdd(&sm.prof[34], (unsigned long long)tqc);   // barrier 1 wait
+    atomicAdd(&sm.prof[33], (unsigned long long)tqb);   // register-pivot publication (incl. its barrier)
+    atomicAdd(&sm.prof[34], (unsigned long long)tqc);   // pivot load + normalisation
     atomicAdd(&sm.prof[35], (unsigned long long)tqd);   // update + local best
     atomicAdd(&sm.prof[36], (unsigned long long)tq1);   // barrier 2 wait
     atomicAdd(&sm.prof[37], (unsigned long long)(prof_clock() - tq0));
@@ -1784,7 +1895,10 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   __syncthreads();
 
   const long long t1 = prof_clock();
-  if (threadIdx.x == 0) sm.sweeps = 0;
+  if (threadIdx.x == 0) {
+    sm.sweeps = 0;
+    sm.kcut = jb.tail_skip ? min(jb.chi_cut, min(M, N)) : MAXDIM;
+  }
   const int Neff = pre ? precond_jacobi(W, cx.X, Mw, Nw, sm, cx.tile, jb.status) : jacobi(W, Mw, Nw, sm, cx.tile, jb.status);
   if (!pre) {
     for (int y = threadIdx.x; y < Mw; y += NT) sm.qpinv[y] = y;
@@ -2372,12 +2486,16 @@ __global__ void __launch_bounds__(NT, 1) expectation_kernel(const double2* buf, 
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int n, double2* Wg, double2* W0g,
                                                     double2* Xg, size_t mat_stride, double* s, double2* u,
-                                                    double2* vh, int* status, unsigned long long* prof, int precond) {
+                                                    double2* vh, int* status, unsigned long long* prof, int precond,
+                                                    int kcut) {
   extern __shared__ double2 dyn_smem[];
   __shared__ Smem sm;
-  if (threadIdx.x == 0) sm.prof = prof;
   const int b = blockIdx.x;
   const int K = min(m, n);
+  if (threadIdx.x == 0) {
+    sm.prof = prof;
+    sm.kcut = (kcut > 0 && kcut < K) ? kcut : MAXDIM;
+  }
   double2* W = Wg + mat_stride * b;
   double2* W0 = W0g + mat_stride * b;
   double2* X = Xg + mat_stride * b;
@@ -2553,6 +2671,8 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
   {
     const char* pe = getenv("TB_PRECOND");
     job.precond = pe ? atoi(pe) : 1;
+    const char* ts = getenv("TB_TAIL_SKIP");
+    job.tail_skip = ts ? atoi(ts) : 1;
   }
   job.floor = d->svalue_floor;
   job.n_samples = d->n_samples;
@@ -2841,6 +2961,11 @@ int tb_expectation(tb_ctx* c, const double* buf, int64_t n, int64_t cap, const i
 }
 
 int tb_svd(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n, double* s, double* u, double* vh) {
+  return tb_svd_trunc(c, a, batch, m, n, 0, s, u, vh);
+}
+
+int tb_svd_trunc(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n, int64_t kcut, double* s, double* u,
+                 double* vh) {
   if (!c) return TB_EINVAL;
   if (!a || !s || batch < 1 || m < 1 || n < 1) return fail(c, TB_EINVAL, "bad arguments");
   if (m > tb::MAXDIM || n > tb::MAXDIM) return fail(c, TB_EINVAL, "matrix larger than 256");
@@ -2862,7 +2987,7 @@ int tb_svd(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n, doub
   const char* pe = getenv("TB_PRECOND");
   const int precond = pe ? atoi(pe) : 1;
   tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->X, c->mat_stride, ds, du, dvh,
-                                               c->dscratch + 1, c->dprof, precond);
+                                               c->dscratch + 1, c->dprof, precond, (int)kcut);
   TB_CUDA(c, cudaGetLastError());
   TB_CUDA(c, cudaDeviceSynchronize());
   TB_CUDA(c, cudaMemcpy(s, ds, batch * k * sizeof(double), cudaMemcpyDeviceToHost));

@@ -66,6 +66,43 @@ def _check_svd(engine, m, n):
         assert np.abs(uu.conj().T @ uu - np.eye(uu.shape[1])).max() < 1e-12
 
 
+# truncated splits (tail skipping): only the kcut kept triplets must be those
+# of the full SVD; spectrum shaped like a saturated chi=64 bond (kept values
+# graded to 1e-10, a tail of ~1e-11 .. 1e-14 values, an exact null space)
+@pytest.mark.parametrize("m,n,kcut", [(128, 128, 64), (64, 64, 32), (128, 64, 16), (64, 128, 40), (256, 256, 128),
+                                      (200, 256, 100)])
+def test_truncated_svd_keeps_exact_triplets(engine, m, n, kcut):
+    lib, ctx = engine.load(), engine.context(0)
+    rng = np.random.default_rng(7 * m + n + kcut)
+    k = min(m, n)
+    mats = []
+    for b in range(3):
+        q1, _ = np.linalg.qr(rng.normal(size=(m, k)) + 1j * rng.normal(size=(m, k)))
+        q2, _ = np.linalg.qr(rng.normal(size=(n, k)) + 1j * rng.normal(size=(n, k)))
+        sv = np.concatenate([np.logspace(0, -10, kcut), 10.0 ** rng.uniform(-14, -10.5, k - kcut)])
+        sv[-(k // 10):] = 0.0
+        if b == 2:  # the tail is the whole spectrum's second half at 1e-3: T stays small or empty
+            sv[kcut:] = 1e-3 * rng.uniform(size=k - kcut)
+        mats.append((q1 * sv) @ q2.conj().T)
+    a = np.ascontiguousarray(np.stack(mats))
+    s = np.zeros((3, k))
+    u = np.zeros((3, m, k), np.complex128)
+    vh = np.zeros((3, k, n), np.complex128)
+    engine.check(lib.tb_svd_trunc(ctx, a.ctypes.data, 3, m, n, kcut, s.ctypes.data, u.ctypes.data, vh.ctypes.data),
+                 ctx)
+    for b in range(3):
+        uu, ref, vv = np.linalg.svd(a[b], full_matrices=False)
+        fro2 = np.linalg.norm(a[b]) ** 2
+        np.testing.assert_allclose(s[b, :kcut] / ref[0], ref[:kcut] / ref[0], rtol=0, atol=1e-13)
+        assert abs(np.sum(s[b] ** 2) - fro2) <= 1e-12 * fro2
+        best = (uu[:, :kcut] * ref[:kcut]) @ vv[:kcut]
+        mine = (u[b][:, :kcut] * s[b, :kcut]) @ vh[b][:kcut]
+        assert np.linalg.norm(mine - best) <= 1e-12 * np.linalg.norm(a[b])
+        live = s[b, :kcut] > 1e-10 * s[b][0]
+        ul = u[b][:, :kcut][:, live]
+        assert np.abs(ul.conj().T @ ul - np.eye(ul.shape[1])).max() < 1e-12
+
+
 def test_single_gate_known_answers(engine, golden):
     kat = golden("ref_kat.npz")
     st = tb.init_product_state("+++")

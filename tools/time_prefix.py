@@ -35,3 +35,5 @@ print("qrcp calls %d avg steps %.1f cyc/step %.0f | within %.3f cross %.3f of to
     pr[8], pr[15]/max(pr[8],1), pr[12]/max(pr[15],1), pr[13]/tot, pr[14]/tot))
 print("Mw=128 cycles per sweep index (k cycles):", [int(pr[40+k]/max(pr[56+min(k,7)],1)/1e3) for k in range(8)], "counts", pr[56:64].astype(int).tolist())
 print("jacobi overheads (share of total): build_l %.3f staging %.3f refresh %.3f swap %.3f writeback %.3f sort_sigma %.3f" % tuple(pr[24:30] / tot))
+print("qrcp sub-phases (cycles/step, thread 0 view): pivot %.0f publish %.0f normalise %.0f update %.0f barrier %.0f" % tuple(
+    pr[32:37] / max(pr[15], 1)))

@@ -125,7 +125,7 @@ struct Smem {
   unsigned char chg[MAXDIM]; // bit0: rotated in the previous sweep, bit1: in this sweep, bit2: tail column
   int jncol[4];              // live columns per Jacobi block slot
   int wbidx[32];
-  double nref[MAXDIM];
+  double nref[MAXDIM];       // QRCP reference norms; after the Jacobi: 1 / sigma of the kept columns
   int qperm[MAXDIM];
   int qpinv[MAXDIM];
   int perm[MAXDIM];
@@ -166,6 +166,94 @@ __device__ double cta_sum(double v, Smem& sm) {
   t = sm.red[NWARP];
   __syncthreads();
   return t;
+}
+
+// ----------------------------------------------------------------------------
+// FP64 tensor-core MMA (DMMA): D(8x8) = A(8x4, row) B(4x8, col) + C.
+// Fragments (lane l): A[l/4][l%4], B[l%4][l/4], C/D[l/4][2(l%4) + {0,1}].
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// ----------------------------------------------------------------------------
+// Tensor-core variant of cta_gemm (below), used for the two hot GEMMs of the
+// two-site update (theta = A.B and the projection Q^H theta).  Same staging
+// and interface; the products run on the FP64 tensor cores: each of the 16 warps owns a 16x16 complex block
+// (2x2 DMMA tiles), a complex MAC being four real m8n8k4 MMAs
+// (re += Ar Br - Ai Bi, im += Ar Bi + Ai Br).  The remaining (small, cold)
+// GEMMs stay on the SIMT version: instantiating the DMMA code at every call
+// site measurably worsened the register allocation of the QRCP/Jacobi
+// functions compiled into the same kernel (QRCP 7.7k -> 9.9k cycles/step).
+// ----------------------------------------------------------------------------
+template <bool AKF, bool BKF, class LA, class LB, class SC>
+__device__ void cta_gemm_tc(int M, int N, int K, LA la, LB lb, SC sc, double2* tile) {
+  double2* As = tile;             // [TK][TLD]  (k rows, m cols)
+  double2* Bs = tile + TK * TLD;  // [TK][TLD]  (k rows, n cols)
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 2) * 16, wn = (warp & 3) * 16;  // warp block inside the 64x64 tile
+  const int fr = lane >> 2, fk = lane & 3;                 // fragment row / k index
+  for (int m0 = 0; m0 < M; m0 += TM) {
+    for (int n0 = 0; n0 < N; n0 += TM) {
+      double cre[2][2][2], cim[2][2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) cre[i][j][e] = cim[i][j][e] = 0.0;
+      for (int k0 = 0; k0 < K; k0 += TK) {
+#pragma unroll
+        for (int e0 = 0; e0 < TK * TM; e0 += NT) {
+          const int e = e0 + tid;
+          int mm, kk;
+          if (AKF) { kk = e & (TK - 1); mm = e / TK; } else { mm = e & (TM - 1); kk = e / TM; }
+          const int gm = m0 + mm, gk = k0 + kk;
+          As[kk * TLD + mm] = (gm < M && gk < K) ? la(gm, gk) : cz();
+          int nn;
+          if (BKF) { kk = e & (TK - 1); nn = e / TK; } else { nn = e & (TM - 1); kk = e / TM; }
+          const int gn = n0 + nn, gk2 = k0 + kk;
+          Bs[kk * TLD + nn] = (gn < N && gk2 < K) ? lb(gk2, gn) : cz();
+        }
+        __syncthreads();
+        const int ksteps = (min(TK, K - k0) + 3) >> 2;
+#pragma unroll 1
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const int kr = (ks * 4 + fk) * TLD;
+          double2 a[2], b[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) a[i] = As[kr + wm + 8 * i + fr];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) b[j] = Bs[kr + wn + 8 * j + fr];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const double nai = -a[i].y;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma(cre[i][j][0], cre[i][j][1], a[i].x, b[j].x);
+              dmma(cre[i][j][0], cre[i][j][1], nai, b[j].y);
+              dmma(cim[i][j][0], cim[i][j][1], a[i].x, b[j].y);
+              dmma(cim[i][j][0], cim[i][j][1], a[i].y, b[j].x);
+            }
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int gm = m0 + wm + 8 * i + fr, gn = n0 + wn + 8 * j + 2 * fk + e;
+            if (gm < M && gn < N) sc(gm, gn, make_double2(cre[i][j][e], cim[i][j][e]));
+          }
+    }
+  }
+  __syncthreads();
 }
 
 // ----------------------------------------------------------------------------
@@ -1830,7 +1918,7 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   const int ldw = orient ? M : N;
 
   // theta = A (2cl x cm) . B (cm x 2cr), written into W
-  cta_gemm<true, false>(
+  cta_gemm_tc<true, false>(
       M, N, cm, [&](int m, int k) { return A[(size_t)m * cap + k]; },
       [&](int k, int n) {
         const int j = n / cr, r = n - j * cr;
@@ -1947,11 +2035,13 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   __syncthreads();
   const int k = sm.k;
   const double scale = sm.scale;
+  for (int c = threadIdx.x; c < k; c += NT) sm.nref[c] = 1.0 / sm.sig[sm.perm[c]];
+  __syncthreads();
   // isometric factor Q[:, c] = W[:, perm c] / sigma
   for (int e = threadIdx.x; e < k * Mw; e += NT) {
     const int c = e / Mw, y = e - c * Mw;
     const int pc = sm.perm[c];
-    const double2 q = cscale(W[(size_t)pc * Mw + sm.qpinv[y]], 1.0 / sm.sig[pc]);
+    const double2 q = cscale(W[(size_t)pc * Mw + sm.qpinv[y]], sm.nref[c]);
     if (merge_right) {
       A[(size_t)y * cap + c] = q;  // site s [(l,i)][c]
     } else {
@@ -1960,12 +2050,9 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
     }
   }
   // weighted factor P = Q^H W0 (k x Nw), scaled by 1/sqrt(kept)
-  cta_gemm<true, true>(
+  cta_gemm_tc<true, true>(
       k, Nw, Mw,
-      [&](int c, int y) {
-        const int pc = sm.perm[c];
-        return cscale(cconj(W[(size_t)pc * Mw + sm.qpinv[y]]), 1.0 / sm.sig[pc]);
-      },
+      [&](int c, int y) { return cscale(cconj(W[(size_t)sm.perm[c] * Mw + sm.qpinv[y]]), sm.nref[c]); },
       [&](int y, int x) { return W0[(size_t)x * Mw + y]; },
       [&](int c, int x, double2 v) {
         if (merge_right) {

@@ -78,6 +78,7 @@ struct Job {
   int n, cap, chi_cut, pi_local;
   int precond;  // QR-preconditioned Jacobi for problems >= 32 x 32
   int tail_skip;  // skip pairs of discarded-tail columns (see mark_tail)
+  int qrcp_tmem;  // QR preconditioner with the matrix in tensor memory (qrcp_tmem)
   double floor;
   int n_samples, n_ckpt, n_obs;
   const uint32_t* gates;
@@ -140,6 +141,8 @@ struct Smem {
   int flag;
   int sweeps;
   int rotcount;
+  uint32_t tmem;             // TMEM base address (512 columns, allocated per CTA)
+  int tmem_on;               // QRCP in tensor memory (qrcp_tmem)
   int kcut;                  // singular triplets the caller keeps (min(chi_cut, K)); tail pairs beyond are skipped
   int ntail;                 // columns currently marked as tail (chg bit 2)
   unsigned long long* prof;
@@ -445,6 +448,12 @@ __device__ void sort_sigma(const double2* W, int Mw, int Nw, Smem& sm) {
 }
 
 __device__ __forceinline__ long long prof_clock() { return clock64(); }
+// per-step clocks inside the QRCP loop: a clock64 read per sub-phase costs a
+// few % of the loop, so they are compiled in only for phase studies
+#ifndef TB_PHASE_CLOCKS
+#define TB_PHASE_CLOCKS 0
+#endif
+__device__ __forceinline__ long long prof_fine() { return TB_PHASE_CLOCKS ? clock64() : 0ll; }
 
 constexpr int JB = 32;  // columns per block
 
@@ -1543,9 +1552,9 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
   const double dead = sm.scale;
   const int rmax = min(Mw, Nw);
   int j = 0;
-  long long tq0 = prof_clock(), tq1 = 0, tq2 = 0, tq3 = 0, tqa = 0, tqb = 0, tqc = 0, tqd = 0;
+  long long tq0 = prof_fine(), tq1 = 0, tq2 = 0, tq3 = 0, tqa = 0, tqb = 0, tqc = 0, tqd = 0;
   for (; j < rmax; ++j) {
-    const long long tt0 = prof_clock();
+    const long long tt0 = prof_fine();
     // global pivot (every warp): largest residual.  Key = high word of the
     // (non-negative) norm with its 7 low bits replaced by 127 - column, so one
     // redux.max picks the largest norm (to ~1e-6 relative; near-ties go to the
@@ -1556,7 +1565,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
     if (kmax == 0u) break;
     const int p = 127 - (int)(kmax & 127u);
-    const long long tt1 = prof_clock();
+    const long long tt1 = prof_fine();
     tqa += tt1 - tt0;
     // Every half normalises the pivot column itself (bit-identical results),
     // reading it straight from its shared-memory home; only a register-held
@@ -1572,7 +1581,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
       __syncthreads();
       src = qaddr;
     }
-    const long long tt2 = prof_clock();
+    const long long tt2 = prof_fine();
     HCol<HR> qv;
     hcol_lds(qv, src);
     {
@@ -1580,7 +1589,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
 #pragma unroll
       for (int q = 0; q < HR; ++q) nn += abs2(qv.v[q]);
       nn = half_sum(nn);
-      const double rn = sqrt(nn), inv = 1.0 / rn;
+      const double inv = rsqrt_nr(nn), rn = nn * inv;
 #pragma unroll
       for (int q = 0; q < HR; ++q) qv.v[q] = cscale(qv.v[q], inv);
       if (hw == owner && hl == 0) {
@@ -1588,7 +1597,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
         sm.qperm[j] = p;
       }
     }
-    const long long tt3 = prof_clock();
+    const long long tt3 = prof_fine();
     tqb += tt2 - tt1;
     tqc += tt3 - tt2;
     // MGS update of one column per half: r = q^H y, y -= r q
@@ -1643,10 +1652,10 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     if (hw == owner && hl == 0) sm.nrm[p] = -1.0;
     __syncwarp();
     local_best();
-    const long long tt4 = prof_clock();
+    const long long tt4 = prof_fine();
     __syncthreads();
     tqd += tt4 - tt3;
-    tq1 += prof_clock() - tt4;
+    tq1 += prof_fine() - tt4;
   }
   if (threadIdx.x == 0 && sm.prof) {
     atomicAdd(&sm.prof[15], (unsigned long long)j);
@@ -1655,7 +1664,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     atomicAdd(&sm.prof[34], (unsigned long long)tqc);   // pivot load + normalisation
     atomicAdd(&sm.prof[35], (unsigned long long)tqd);   // update + local best
     atomicAdd(&sm.prof[36], (unsigned long long)tq1);   // barrier 2 wait
-    atomicAdd(&sm.prof[37], (unsigned long long)(prof_clock() - tq0));
+    atomicAdd(&sm.prof[37], (unsigned long long)(prof_fine() - tq0));
   }
   (void)tq2; (void)tq3;
   // complete the permutation with the numerically dead columns
@@ -1663,6 +1672,192 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     int k = j;
     for (int c = 0; c < Mw; ++c)
       if (sm.nrm[c] >= 0.0) sm.qperm[k++] = c;
+    for (int k2 = 0; k2 < Mw; ++k2) sm.qpinv[sm.qperm[k2]] = k2;
+  }
+  __syncthreads();
+  return j;
+}
+
+// TMEM allocation of the whole 512-column tensor memory of the SM (one CTA
+// per SM); qrcp_tmem is its only user.
+__device__ __forceinline__ void tmem_alloc(Smem& sm) {
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+}
+__device__ __forceinline__ void tmem_free(Smem& sm) {
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(sm.tmem));
+}
+
+// ----------------------------------------------------------------------------
+// TMEM-resident column-pivoted MGS (same algorithm and outputs as qrcp_mgs).
+// Y (Nw <= 128 rows x Mw <= 128 columns) lives in tensor memory: TMEM lane c
+// holds column c, words 4y..4y+3 its row y (re.lo, re.hi, im.lo, im.hi) —
+// 128 lanes x 512 words is exactly one 128 x 128 complex128 matrix.  Warp w
+// reaches the lanes of quadrant w & 3, so thread (w, l) owns column
+// 32 (w & 3) + l and rows 32 (w >> 2) .. +32: dot products need no shuffles,
+// only a 4-way combination of row-group partials through shared memory, and
+// the shared-memory traffic of a step is just the pivot column (broadcast
+// reads) instead of every column's load + store.  Column norms are recomputed
+// exactly every step from the partials of the update pass.  Three barriers
+// per step: q published, dot partials, norm partials.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void tm_ld32(uint32_t a, uint32_t (&v)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]) : "r"(a) : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_st32(uint32_t a, const uint32_t (&v)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" :: "r"(a), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ double2 tm_c(const uint32_t (&v)[32], int r) {
+  return make_double2(__hiloint2double((int)v[4 * r + 1], (int)v[4 * r]), __hiloint2double((int)v[4 * r + 3], (int)v[4 * r + 2]));
+}
+__device__ __forceinline__ void tm_put(uint32_t (&v)[32], int r, double2 e) {
+  v[4 * r] = (uint32_t)__double2loint(e.x);
+  v[4 * r + 1] = (uint32_t)__double2hiint(e.x);
+  v[4 * r + 2] = (uint32_t)__double2loint(e.y);
+  v[4 * r + 3] = (uint32_t)__double2hiint(e.y);
+}
+
+__device__ __noinline__ int qrcp_tmem(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, double2* smem) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q4 = w & 3, g = w >> 2;
+  const int c = 32 * q4 + lane;
+  const bool colok = c < Mw;
+  const uint32_t tb = sm.tmem + ((uint32_t)(32 * q4) << 16) + 128u * g;
+  double2* qbuf = smem;                              // [128] pivot column (unnormalised)
+  double2* dpart = smem + 128;                       // [4][128] dot partials
+  double* npart = reinterpret_cast<double*>(smem + 128 + 512);  // [4][128] norm partials
+  // stage Y into TMEM, partial norms
+  {
+    double pn = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+      uint32_t v[32];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int y = 32 * g + 8 * k + r;
+        const double2 e = (colok && y < Nw) ? Y[(size_t)c * Nw + y] : cz();
+        pn += abs2(e);
+        tm_put(v, r, e);
+      }
+      tm_st32(tb + 32u * k, v);
+    }
+    tm_wait_st();
+    npart[g * 128 + c] = pn;
+    if (g == 0) sm.nrm[c] = colok ? 0.0 : -1.0;  // alive flag (>= 0)
+  }
+  __syncthreads();
+  // dead threshold on the residual norm^2 (1e-28 of |Y|_F^2)
+  if (threadIdx.x < 32) {
+    double t = 0.0;
+    for (int cc = threadIdx.x; cc < Mw; cc += 32)
+      t += ((npart[cc] + npart[128 + cc]) + (npart[256 + cc] + npart[384 + cc]));
+    t = warp_sum(t);
+    if (threadIdx.x == 0) sm.scale = 1e-28 * t;
+  }
+  __syncthreads();
+  const double dead = sm.scale;
+  const int rmax = min(Mw, Nw);
+  int j = 0;
+  for (; j < rmax; ++j) {
+    // pivot (every warp, redundantly): exact residual norms from the partials
+    unsigned key = 0u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int cc = lane + 32 * t;
+      if (cc < Mw && sm.nrm[cc] >= 0.0) {
+        const double nn = (npart[cc] + npart[128 + cc]) + (npart[256 + cc] + npart[384 + cc]);
+        if (nn > dead) key = max(key, ((unsigned)__double2hiint(nn) & 0xFFFFFF80u) | (unsigned)(127 - cc));
+      }
+    }
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+    if (kmax == 0u) break;
+    const int p = 127 - (int)(kmax & 127u);
+    const double nn = (npart[p] + npart[128 + p]) + (npart[256 + p] + npart[384 + p]);
+    const double inv = rsqrt_nr(nn), rn = nn * inv;
+    // the owners of column p publish it (tcgen05.ld is warp-collective: the
+    // four warps of p's quadrant load, lane p % 32 writes)
+    if (q4 == (p >> 5)) {
+#pragma unroll 1
+      for (int k = 0; k < 4; ++k) {
+        uint32_t v[32];
+        tm_ld32(tb + 32u * k, v);
+        if (c == p) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) qbuf[32 * g + 8 * k + r] = tm_c(v, r);
+        }
+      }
+      if (c == p && g == 0) {
+        R[(size_t)j * Mw + p] = make_double2(rn, 0.0);
+        sm.qperm[j] = p;
+      }
+    }
+    const bool alive = colok && c != p && sm.nrm[c] >= 0.0;
+    __syncthreads();  // B1: q published; every alive-flag read done
+    if (c == p && g == 0) sm.nrm[p] = -1.0;
+    // dot partial: y_p^H y_c over my rows
+    // (every TMEM access below is executed by whole warps; dead columns
+    // compute on their data and discard the result / store it back unchanged)
+    const bool wany = __any_sync(0xffffffffu, alive);
+    double2 d = cz();
+    if (wany) {
+      double2 e2 = cz();
+#pragma unroll 1
+      for (int k = 0; k < 4; ++k) {
+        uint32_t v[32];
+        tm_ld32(tb + 32u * k, v);
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) {
+          cfmac(d, qbuf[32 * g + 8 * k + r], tm_c(v, r));
+          cfmac(e2, qbuf[32 * g + 8 * k + r + 1], tm_c(v, r + 1));
+        }
+      }
+      d = cadd(d, e2);
+    }
+    dpart[g * 128 + c] = alive ? d : cz();
+    __syncthreads();  // B2: dot partials
+    double pn = 0.0;
+    if (wany) {
+      const double2 s0 = cadd(cadd(dpart[c], dpart[128 + c]), cadd(dpart[256 + c], dpart[384 + c]));
+      const double2 rr = cscale(s0, inv);                // r = q^H y
+      const double2 f = alive ? cscale(rr, inv) : cz();  // y -= r q = (r / rn) y_p
+      if (alive && g == 0) R[(size_t)j * Mw + c] = rr;
+#pragma unroll 1
+      for (int k = 0; k < 4; ++k) {
+        uint32_t v[32];
+        tm_ld32(tb + 32u * k, v);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          double2 y = tm_c(v, r);
+          const double2 qy = qbuf[32 * g + 8 * k + r];
+          y.x -= f.x * qy.x - f.y * qy.y;
+          y.y -= f.x * qy.y + f.y * qy.x;
+          pn += abs2(y);
+          tm_put(v, r, y);
+        }
+        tm_st32(tb + 32u * k, v);
+      }
+      tm_wait_st();
+    }
+    npart[g * 128 + c] = alive ? pn : 0.0;
+    __syncthreads();  // B3: norm partials (and the dead flag of p)
+  }
+  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
+  // complete the permutation with the numerically dead columns
+  if (threadIdx.x == 0) {
+    int k = j;
+    for (int cc = 0; cc < Mw; ++cc)
+      if (sm.nrm[cc] >= 0.0) sm.qperm[k++] = cc;
     for (int k2 = 0; k2 < Mw; ++k2) sm.qpinv[sm.qperm[k2]] = k2;
   }
   __syncthreads();
@@ -1682,7 +1877,7 @@ __device__ void build_l(const double2* R, int Mw, int r, double2* W, const Smem&
 template <int HR>
 __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
   const long long t0 = prof_clock();
-  const int r = qrcp_mgs<HR>(W, Nw, Mw, X, sm, smem);
+  const int r = (sm.tmem_on && HR == 8) ? qrcp_tmem(W, Nw, Mw, X, sm, smem) : qrcp_mgs<HR>(W, Nw, Mw, X, sm, smem);
   if (threadIdx.x == 0 && sm.prof) {
     atomicAdd(&sm.prof[12], (unsigned long long)(prof_clock() - t0));
     atomicAdd(&sm.prof[8], 1ull);
@@ -1917,23 +2112,39 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   const bool orient = pre ? !merge_right : merge_right;  // true: col-major theta
   const int ldw = orient ? M : N;
 
-  // theta = A (2cl x cm) . B (cm x 2cr), written into W
+  // theta = A (2cl x cm) . B (cm x 2cr), written into W.  A swap (_kernel.py:
+  // 171-181) only exchanges the physical legs, theta'[(l,j),(i,r)] =
+  // theta[(l,i),(j,r)], so the GEMM epilogue writes it straight to its
+  // permuted place in both W and W0; a gate needs the pass below.
+  const bool swap = kind == 1;
   cta_gemm_tc<true, false>(
       M, N, cm, [&](int m, int k) { return A[(size_t)m * cap + k]; },
       [&](int k, int n) {
-        const int j = n / cr, r = n - j * cr;
-        return B[(size_t)(k * 2 + j) * cap + r];
+        const int j = n >= cr ? 1 : 0;  // n < 2 cr
+        return B[(size_t)(k * 2 + j) * cap + (n - j * cr)];
       },
       [&](int m, int n, double2 v) {
-        if (orient) W[(size_t)n * ldw + m] = v;
-        else W[(size_t)m * ldw + n] = cconj(v);
+        int row = m, col = n;
+        if (swap) {
+          const int j = n >= cr ? 1 : 0, r = n - j * cr;
+          row = (m & ~1) | j;
+          col = (m & 1) * cr + r;
+          W0[merge_right ? (size_t)col * Mw + row : (size_t)row * Mw + col] = merge_right ? v : cconj(v);
+        }
+        if (orient) W[(size_t)col * ldw + row] = v;
+        else W[(size_t)row * ldw + col] = cconj(v);
       },
       cx.tile);
+  const long long tg = prof_clock();
+  prof_add(jb, 30, tg - t0);
 
-  // gate / swap on the physical pair, fused into the (W, W0) write-out
+  // gate on the physical pair, fused into the (W, W0) write-out
   const int fa = (pa == 3) ? 0 : 1, fb = (pb == 3) ? 0 : 1;
-  for (int e = threadIdx.x; e < cl * cr; e += NT) {
-    const int l = e / cr, r = e - (e / cr) * cr;
+  for (int e = swap ? cl * cr : threadIdx.x; e < cl * cr; e += NT) {
+    // consecutive threads walk the contiguous index of W's layout
+    int l, r;
+    if (orient) { r = e / cl; l = e - r * cl; }
+    else { l = e / cr; r = e - l * cr; }
     double2 t[2][2];
     size_t idx[2][2];
     size_t idw[2][2];
@@ -1983,6 +2194,7 @@ __device__ void two_site(const Ctx& cx, Smem& sm, int s, int kind, int pa, int p
   __syncthreads();
 
   const long long t1 = prof_clock();
+  prof_add(jb, 31, t1 - tg);
   if (threadIdx.x == 0) {
     sm.sweeps = 0;
     sm.kcut = jb.tail_skip ? min(jb.chi_cut, min(M, N)) : MAXDIM;
@@ -2402,7 +2614,9 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
   if (threadIdx.x == 0) {
     sm.flops = 0.0;
     sm.prof = job.prof;
+    sm.tmem_on = job.qrcp_tmem;
   }
+  if (job.qrcp_tmem) tmem_alloc(sm);
   for (int iter = 0;; ++iter) {
     if (job.slot_mode) {
       if (iter > 0 || (int)blockIdx.x >= job.n_samples) break;
@@ -2517,6 +2731,7 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
     __syncthreads();
   }
   if (threadIdx.x == 0) job.flops[blockIdx.x] += sm.flops;
+  if (job.qrcp_tmem) tmem_free(sm);
 }
 
 // ----------------------------------------------------------------------------
@@ -2582,12 +2797,14 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
   if (threadIdx.x == 0) {
     sm.prof = prof;
     sm.kcut = (kcut > 0 && kcut < K) ? kcut : MAXDIM;
+    sm.tmem_on = (precond >> 1) & 1;
   }
+  if (precond & 2) tmem_alloc(sm);
   double2* W = Wg + mat_stride * b;
   double2* W0 = W0g + mat_stride * b;
   double2* X = Xg + mat_stride * b;
   const double2* A = a + (size_t)b * m * n;
-  const bool pre = precond && m >= 32 && n >= 32;
+  const bool pre = (precond & 1) && m >= 32 && n >= 32;
   // left singular vectors of A (m x n): columns of W = A, or Y = A^H when preconditioned
   for (int e = threadIdx.x; e < m * n; e += NT) {
     const int y = e / n, c = e - y * n;
@@ -2623,6 +2840,7 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
         },
         [&](int y, int x) { return W0[(size_t)x * m + y]; },
         [&](int c, int x, double2 v) { vh[(size_t)b * K * n + (size_t)c * n + x] = v; }, dyn_smem);
+  if (precond & 2) tmem_free(sm);
 }
 
 constexpr size_t kTileBytes = 2 * TK * TLD * sizeof(double2);
@@ -2760,6 +2978,8 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
     job.precond = pe ? atoi(pe) : 1;
     const char* ts = getenv("TB_TAIL_SKIP");
     job.tail_skip = ts ? atoi(ts) : 1;
+    const char* tm = getenv("TB_QRCP_TMEM");
+    job.qrcp_tmem = tm ? atoi(tm) : 0;
   }
   job.floor = d->svalue_floor;
   job.n_samples = d->n_samples;
@@ -3072,7 +3292,8 @@ int tb_svd_trunc(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n
   const size_t smem = tb::kDynSmem;
   TB_CUDA(c, cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const char* pe = getenv("TB_PRECOND");
-  const int precond = pe ? atoi(pe) : 1;
+  const char* tm = getenv("TB_QRCP_TMEM");
+  const int precond = (pe ? atoi(pe) : 1) | ((tm && atoi(tm)) ? 2 : 0);
   tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->X, c->mat_stride, ds, du, dvh,
                                                c->dscratch + 1, c->dprof, precond, (int)kcut);
   TB_CUDA(c, cudaGetLastError());

@@ -45,6 +45,14 @@ def test_wide_svd_matches_lapack(engine, monkeypatch, m, n, precond):
     _check_svd(engine, m, n)
 
 
+# QR preconditioner with the matrix in tensor memory (TB_QRCP_TMEM=1): same
+# parity bar on the half-warp (<= 128) shapes it serves
+@pytest.mark.parametrize("m,n", [(32, 32), (64, 128), (128, 64), (128, 128), (100, 77), (128, 96)])
+def test_tmem_qrcp_svd_matches_lapack(engine, monkeypatch, m, n):
+    monkeypatch.setenv("TB_QRCP_TMEM", "1")
+    _check_svd(engine, m, n)
+
+
 def _check_svd(engine, m, n):
     rng = np.random.default_rng(m * 1000 + n)
     k = min(m, n)
@@ -225,7 +233,9 @@ def test_c1_estimator_vs_reference_mean(engine, golden):
     np.testing.assert_allclose(run.values[:, :, 0], ref["z0"], atol=1e-10)
 
 
-def test_c2_truncated_prefix_parity(engine, golden):
+@pytest.mark.parametrize("tmem", ["0", "1"])
+def test_c2_truncated_prefix_parity(engine, golden, monkeypatch, tmem):
+    monkeypatch.setenv("TB_QRCP_TMEM", tmem)
     ref = golden("ref_c2.npz")
     ham = tb.build_spin_ring(16, 1.0, 2)
     cfg = tb.PaiConfig(DELTA, 200, 2.0)
@@ -241,7 +251,9 @@ def test_c2_truncated_prefix_parity(engine, golden):
         np.testing.assert_allclose(run.discarded[i][ok], ref["disc"][i][:4][ok], rtol=0.25, atol=1e-13)
 
 
-def test_c3_headline_prefix_parity(engine, golden):
+@pytest.mark.parametrize("tmem", ["0", "1"])
+def test_c3_headline_prefix_parity(engine, golden, monkeypatch, tmem):
+    monkeypatch.setenv("TB_QRCP_TMEM", tmem)
     ref = golden("ref_c3.npz")
     ham = tb.build_spin_ring(32, 1.0, 4)
     cfg = tb.PaiConfig(DELTA, 200, 2.0)

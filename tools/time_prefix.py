@@ -37,3 +37,4 @@ print("Mw=128 cycles per sweep index (k cycles):", [int(pr[40+k]/max(pr[56+min(k
 print("jacobi overheads (share of total): build_l %.3f staging %.3f refresh %.3f swap %.3f writeback %.3f sort_sigma %.3f" % tuple(pr[24:30] / tot))
 print("qrcp sub-phases (cycles/step, thread 0 view): pivot %.0f publish %.0f normalise %.0f update %.0f barrier %.0f" % tuple(
     pr[32:37] / max(pr[15], 1)))
+print("two-site front end (share of total): theta GEMM %.3f gate pass %.3f" % (pr[30] / tot, pr[31] / tot))

@@ -1698,17 +1698,18 @@ __device__ __forceinline__ void tmem_free(Smem& sm) {
 }
 
 // ----------------------------------------------------------------------------
-// TMEM-resident column-pivoted MGS (same algorithm and outputs as qrcp_mgs).
-// Y (Nw <= 128 rows x Mw <= 128 columns) lives in tensor memory: TMEM lane c
-// holds column c, words 4y..4y+3 its row y (re.lo, re.hi, im.lo, im.hi) —
-// 128 lanes x 512 words is exactly one 128 x 128 complex128 matrix.  Warp w
-// reaches the lanes of quadrant w & 3, so thread (w, l) owns column
-// 32 (w & 3) + l and rows 32 (w >> 2) .. +32: dot products need no shuffles,
-// only a 4-way combination of row-group partials through shared memory, and
-// the shared-memory traffic of a step is just the pivot column (broadcast
-// reads) instead of every column's load + store.  Column norms are recomputed
-// exactly every step from the partials of the update pass.  Three barriers
-// per step: q published, dot partials, norm partials.
+// TMEM-resident column-pivoted MGS (same algorithm, layout and outputs as
+// qrcp_mgs<8>).  The smem version is bound by shared-memory bandwidth: every
+// live column is loaded and stored once per step (4 KB each, ~3k of its ~7.5k
+// cycles per step at 128 B/clk).  Here the columns live in tensor memory,
+// which streams at ~470 B/clk (ld) / ~970 B/clk (st) per SM on this B200
+// (tools/tmem_bw.cu).  Half-warp k owns columns k + 32 t (t = 0..3) exactly as
+// in qrcp_mgs: lane l of the half holds rows l + 16 q, i.e. TMEM lane
+// 32 (w & 3) + l' (l' = lane in the warp), words 128 (w >> 2) + 32 t + 4 q —
+// the four warps of a lane quadrant split its 512 words, so all 128 columns
+// fit.  tcgen05.ld/st are warp-collective, so both halves of a warp move
+// their column t together.  The pivot column is published through a 2 KB
+// shared-memory buffer (one extra barrier per step).
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ void tm_ld32(uint32_t a, uint32_t (&v)[32]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]) : "r"(a) : "memory");
@@ -1728,136 +1729,155 @@ __device__ __forceinline__ void tm_put(uint32_t (&v)[32], int r, double2 e) {
   v[4 * r + 3] = (uint32_t)__double2hiint(e.y);
 }
 
-__device__ __noinline__ int qrcp_tmem(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, double2* smem) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int q4 = w & 3, g = w >> 2;
-  const int c = 32 * q4 + lane;
-  const bool colok = c < Mw;
-  const uint32_t tb = sm.tmem + ((uint32_t)(32 * q4) << 16) + 128u * g;
-  double2* qbuf = smem;                              // [128] pivot column (unnormalised)
-  double2* dpart = smem + 128;                       // [4][128] dot partials
-  double* npart = reinterpret_cast<double*>(smem + 128 + 512);  // [4][128] norm partials
-  // stage Y into TMEM, partial norms
-  {
-    double pn = 0.0;
-#pragma unroll 1
-    for (int k = 0; k < 4; ++k) {
-      uint32_t v[32];
+__device__ __forceinline__ void tm_ld_col(uint32_t a, HCol<8>& c) {
+  uint32_t v[32];
+  tm_ld32(a, v);
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int y = 32 * g + 8 * k + r;
-        const double2 e = (colok && y < Nw) ? Y[(size_t)c * Nw + y] : cz();
-        pn += abs2(e);
-        tm_put(v, r, e);
-      }
-      tm_st32(tb + 32u * k, v);
-    }
-    tm_wait_st();
-    npart[g * 128 + c] = pn;
-    if (g == 0) sm.nrm[c] = colok ? 0.0 : -1.0;  // alive flag (>= 0)
+  for (int q = 0; q < 8; ++q) c.v[q] = tm_c(v, q);
+}
+__device__ __forceinline__ void tm_st_col(uint32_t a, const HCol<8>& c) {
+  uint32_t v[32];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tm_put(v, q, c.v[q]);
+  tm_st32(a, v);
+}
+
+__device__ __noinline__ int qrcp_tmem(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, double2* smem) {
+  constexpr int HR = 8;
+  const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t qaddr = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t tcol = sm.tmem + ((uint32_t)(32 * (w & 3)) << 16) + 128u * (uint32_t)(w >> 2);
+  // stage column hw + 32 t into word block t, exact norms
+#pragma unroll 1
+  for (int t = 0; t < 4; ++t) {
+    const int c = hw + 32 * t;
+    HCol<HR> v;
+    hcol_ldg(v, Y + (size_t)c * Nw, c < Mw ? Nw : 0);
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < HR; ++q) acc += abs2(v.v[q]);
+    acc = half_sum(acc);
+    if (hl == 0 && c < Mw) sm.nrm[c] = sm.nref[c] = acc;
+    tm_st_col(tcol + 32u * t, v);
   }
+  tm_wait_st();
   __syncthreads();
-  // dead threshold on the residual norm^2 (1e-28 of |Y|_F^2)
   if (threadIdx.x < 32) {
     double t = 0.0;
-    for (int cc = threadIdx.x; cc < Mw; cc += 32)
-      t += ((npart[cc] + npart[128 + cc]) + (npart[256 + cc] + npart[384 + cc]));
+    for (int c = threadIdx.x; c < Mw; c += 32) t += sm.nrm[c];
     t = warp_sum(t);
-    if (threadIdx.x == 0) sm.scale = 1e-28 * t;
+    if (threadIdx.x == 0) sm.scale = 1e-28 * t;  // dead threshold on residual norm^2
   }
+  auto local_best = [&]() {
+    const int c = hw + 32 * hl;
+    const bool ok = hl < 4 && c < Mw;
+    double best = ok ? sm.nrm[c] : -1.0;
+    int bi = ok ? c : -1;
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
+    }
+    if (hl == 0) {
+      sm.wbest[hw] = best;
+      sm.wbidx[hw] = bi;
+    }
+  };
+  local_best();
   __syncthreads();
   const double dead = sm.scale;
   const int rmax = min(Mw, Nw);
   int j = 0;
   for (; j < rmax; ++j) {
-    // pivot (every warp, redundantly): exact residual norms from the partials
-    unsigned key = 0u;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int cc = lane + 32 * t;
-      if (cc < Mw && sm.nrm[cc] >= 0.0) {
-        const double nn = (npart[cc] + npart[128 + cc]) + (npart[256 + cc] + npart[384 + cc]);
-        if (nn > dead) key = max(key, ((unsigned)__double2hiint(nn) & 0xFFFFFF80u) | (unsigned)(127 - cc));
-      }
-    }
+    const int wi = sm.wbidx[lane];
+    const double wv = sm.wbest[lane];
+    const unsigned key = (wi >= 0 && wv > dead) ? ((unsigned)__double2hiint(wv) & 0xFFFFFF80u) | (unsigned)(127 - wi) : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
     if (kmax == 0u) break;
     const int p = 127 - (int)(kmax & 127u);
-    const double nn = (npart[p] + npart[128 + p]) + (npart[256 + p] + npart[384 + p]);
-    const double inv = rsqrt_nr(nn), rn = nn * inv;
-    // the owners of column p publish it (tcgen05.ld is warp-collective: the
-    // four warps of p's quadrant load, lane p % 32 writes)
-    if (q4 == (p >> 5)) {
-#pragma unroll 1
-      for (int k = 0; k < 4; ++k) {
-        uint32_t v[32];
-        tm_ld32(tb + 32u * k, v);
-        if (c == p) {
+    const int owner = p & 31, tp = p >> 5;
+    if ((owner >> 1) == w) {  // the owner's warp loads (warp-collective), the owner half publishes
+      HCol<HR> v;
+      tm_ld_col(tcol + 32u * tp, v);
+      if (hw == owner) hcol_sts(qaddr, v);
+    }
+    __syncthreads();
+    HCol<HR> qv;
+    hcol_lds(qv, qaddr);
+    {
+      double nn = 0.0;
 #pragma unroll
-          for (int r = 0; r < 8; ++r) qbuf[32 * g + 8 * k + r] = tm_c(v, r);
-        }
-      }
-      if (c == p && g == 0) {
+      for (int q = 0; q < HR; ++q) nn += abs2(qv.v[q]);
+      nn = half_sum(nn);
+      const double inv = rsqrt_nr(nn), rn = nn * inv;
+#pragma unroll
+      for (int q = 0; q < HR; ++q) qv.v[q] = cscale(qv.v[q], inv);
+      if (hw == owner && hl == 0) {
         R[(size_t)j * Mw + p] = make_double2(rn, 0.0);
         sm.qperm[j] = p;
       }
     }
-    const bool alive = colok && c != p && sm.nrm[c] >= 0.0;
-    __syncthreads();  // B1: q published; every alive-flag read done
-    if (c == p && g == 0) sm.nrm[p] = -1.0;
-    // dot partial: y_p^H y_c over my rows
-    // (every TMEM access below is executed by whole warps; dead columns
-    // compute on their data and discard the result / store it back unchanged)
-    const bool wany = __any_sync(0xffffffffu, alive);
-    double2 d = cz();
-    if (wany) {
-      double2 e2 = cz();
-#pragma unroll 1
-      for (int k = 0; k < 4; ++k) {
-        uint32_t v[32];
-        tm_ld32(tb + 32u * k, v);
+    // MGS update of one column per half: r = q^H y, y -= r q.  An invalid
+    // column applies d = 0 and is stored back unchanged.  (Two columns at a
+    // time, to interleave their reductions, spilled in the hot loop: 16.4k
+    // instead of 5.8k cycles per step.)
+    auto dotp = [&](const HCol<HR>& y) {
+      double2 d = cz(), e = cz();
 #pragma unroll
-        for (int r = 0; r < 8; r += 2) {
-          cfmac(d, qbuf[32 * g + 8 * k + r], tm_c(v, r));
-          cfmac(e2, qbuf[32 * g + 8 * k + r + 1], tm_c(v, r + 1));
-        }
+      for (int q = 0; q < HR; q += 2) {
+        cfmac(d, qv.v[q], y.v[q]);
+        cfmac(e, qv.v[q + 1], y.v[q + 1]);
       }
-      d = cadd(d, e2);
-    }
-    dpart[g * 128 + c] = alive ? d : cz();
-    __syncthreads();  // B2: dot partials
-    double pn = 0.0;
-    if (wany) {
-      const double2 s0 = cadd(cadd(dpart[c], dpart[128 + c]), cadd(dpart[256 + c], dpart[384 + c]));
-      const double2 rr = cscale(s0, inv);                // r = q^H y
-      const double2 f = alive ? cscale(rr, inv) : cz();  // y -= r q = (r / rn) y_p
-      if (alive && g == 0) R[(size_t)j * Mw + c] = rr;
-#pragma unroll 1
-      for (int k = 0; k < 4; ++k) {
-        uint32_t v[32];
-        tm_ld32(tb + 32u * k, v);
+      return cadd(d, e);
+    };
+    auto apply = [&](HCol<HR>& y, int c, bool valid, double2 d) {
+      if (!valid) d = cz();
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          double2 y = tm_c(v, r);
-          const double2 qy = qbuf[32 * g + 8 * k + r];
-          y.x -= f.x * qy.x - f.y * qy.y;
-          y.y -= f.x * qy.y + f.y * qy.x;
-          pn += abs2(y);
-          tm_put(v, r, y);
-        }
-        tm_st32(tb + 32u * k, v);
+      for (int q = 0; q < HR; ++q) {
+        y.v[q].x -= d.x * qv.v[q].x - d.y * qv.v[q].y;
+        y.v[q].y -= d.x * qv.v[q].y + d.y * qv.v[q].x;
       }
-      tm_wait_st();
+      double nr = valid ? sm.nrm[c] - abs2(d) : 0.0;
+      const bool f = valid && nr < 1e-2 * sm.nref[c];
+      if (__any_sync(0xffffffffu, f)) {  // cancellation: exact norm
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < HR; ++q) acc += abs2(y.v[q]);
+        acc = half_sum(acc);
+        if (f) nr = acc;
+      }
+      if (hl == 0 && valid) {
+        sm.nrm[c] = nr;
+        if (f) sm.nref[c] = nr;
+        R[(size_t)j * Mw + c] = d;
+      }
+    };
+#pragma unroll 1
+    for (int t = 0; t < 4; ++t) {
+      const int c = hw + 32 * t;
+      const bool valid = c < Mw && c != p && sm.nrm[c] >= 0.0;
+      if (!__any_sync(0xffffffffu, valid)) continue;
+      HCol<HR> y;
+      tm_ld_col(tcol + 32u * t, y);
+      double2 d = dotp(y);
+      d.x = half_sum(d.x);
+      d.y = half_sum(d.y);
+      apply(y, c, valid, d);
+      tm_st_col(tcol + 32u * t, y);
     }
-    npart[g * 128 + c] = alive ? pn : 0.0;
-    __syncthreads();  // B3: norm partials (and the dead flag of p)
+    tm_wait_st();
+    if (hw == owner && hl == 0) sm.nrm[p] = -1.0;
+    __syncwarp();
+    local_best();
+    __syncthreads();
   }
   if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
   // complete the permutation with the numerically dead columns
   if (threadIdx.x == 0) {
     int k = j;
-    for (int cc = 0; cc < Mw; ++cc)
-      if (sm.nrm[cc] >= 0.0) sm.qperm[k++] = cc;
+    for (int c = 0; c < Mw; ++c)
+      if (sm.nrm[c] >= 0.0) sm.qperm[k++] = c;
     for (int k2 = 0; k2 < Mw; ++k2) sm.qpinv[sm.qperm[k2]] = k2;
   }
   __syncthreads();
@@ -2979,7 +2999,7 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
     const char* ts = getenv("TB_TAIL_SKIP");
     job.tail_skip = ts ? atoi(ts) : 1;
     const char* tm = getenv("TB_QRCP_TMEM");
-    job.qrcp_tmem = tm ? atoi(tm) : 0;
+    job.qrcp_tmem = tm ? atoi(tm) : 1;
   }
   job.floor = d->svalue_floor;
   job.n_samples = d->n_samples;
@@ -3293,7 +3313,7 @@ int tb_svd_trunc(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n
   TB_CUDA(c, cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const char* pe = getenv("TB_PRECOND");
   const char* tm = getenv("TB_QRCP_TMEM");
-  const int precond = (pe ? atoi(pe) : 1) | ((tm && atoi(tm)) ? 2 : 0);
+  const int precond = (pe ? atoi(pe) : 1) | ((!tm || atoi(tm)) ? 2 : 0);
   tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->X, c->mat_stride, ds, du, dvh,
                                                c->dscratch + 1, c->dprof, precond, (int)kcut);
   TB_CUDA(c, cudaGetLastError());

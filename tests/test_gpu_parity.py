@@ -45,11 +45,13 @@ def test_wide_svd_matches_lapack(engine, monkeypatch, m, n, precond):
     _check_svd(engine, m, n)
 
 
-# QR preconditioner with the matrix in tensor memory (TB_QRCP_TMEM=1): same
-# parity bar on the half-warp (<= 128) shapes it serves
+# QR preconditioner with the matrix in tensor memory (TB_QRCP_TMEM=1, the
+# default) and the shared-memory variant (0): same parity bar on the
+# half-warp (<= 128) shapes they serve
 @pytest.mark.parametrize("m,n", [(32, 32), (64, 128), (128, 64), (128, 128), (100, 77), (128, 96)])
-def test_tmem_qrcp_svd_matches_lapack(engine, monkeypatch, m, n):
-    monkeypatch.setenv("TB_QRCP_TMEM", "1")
+@pytest.mark.parametrize("tmem", ["0", "1"])
+def test_tmem_qrcp_svd_matches_lapack(engine, monkeypatch, m, n, tmem):
+    monkeypatch.setenv("TB_QRCP_TMEM", tmem)
     _check_svd(engine, m, n)
 
 

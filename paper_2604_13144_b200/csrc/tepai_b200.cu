@@ -500,6 +500,11 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   y = y * fma(-h * y, y, 1.5);
   return y;
 }
+__device__ __forceinline__ double rsqrt_nr1(double x) {  // one Newton step: ~2^-44 relative
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y * fma(-0.5 * x * y, y, 1.5);
+}
 __device__ __forceinline__ double rcp_nr1(double x) {  // ~2^-44 relative
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -519,15 +524,17 @@ __device__ __forceinline__ Rot rot_params(double gr, double gi, double al, doubl
   const double g = gs * ig;
   const double d = be - al;
   const double h2 = fma(d, d, 4.0 * gs);
-  const double h = h2 * rsqrt_nr(h2);
-  const double t = copysign(2.0 * g, d) * rcp_nr1(fabs(d) + h);
+  const double h = h2 * rsqrt_nr1(h2);  // only fixes the angle t (see above)
+  // a pair left alone gets t = 0 and c = 1 (the exact identity: s, tg and the
+  // scaled factors built from t vanish; e stays finite because gs = 1)
+  const double t = rot ? copysign(2.0 * g, d) * rcp_nr1(fabs(d) + h) : 0.0;
   const double c = rsqrt_nr(fma(t, t, 1.0));
   p.c = rot ? c : 1.0;
-  p.s = rot ? t * c : 0.0;
-  p.er = rot ? gr * ig : 1.0;
-  p.ei = rot ? -gi * ig : 0.0;
-  p.tg = rot ? t * g : 0.0;
-  p.t = rot ? t : 0.0;
+  p.s = t * c;
+  p.er = gr * ig;
+  p.ei = -gi * ig;
+  p.tg = t * g;
+  p.t = t;
   return p;
 }
 

@@ -74,7 +74,8 @@ def load() -> ctypes.CDLL:
         lib.tb_run_stream.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp, vp, vp, i64, i64, dbl, vp, vp]
         lib.tb_expectation.argtypes = [vp, vp, i64, i64, vp, vp, vp]
         lib.tb_svd.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp]
-        lib.tb_svd_trunc.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp]
+        if hasattr(lib, "tb_svd_trunc"):  # absent in pre-r01b builds (A/B timing of old libraries)
+            lib.tb_svd_trunc.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp]
         lib.tb_run_ensemble.argtypes = [vp, ctypes.POINTER(EnsembleDesc), ctypes.POINTER(EnsembleOut)]
         lib.tb_run_ensemble_device.argtypes = [vp, ctypes.POINTER(EnsembleDesc), ctypes.POINTER(EnsembleOut), vp]
         lib.tb_step.argtypes = [vp, ctypes.POINTER(StepDesc), ctypes.POINTER(EnsembleOut), i64]

@@ -2,7 +2,8 @@
 Heisenberg ring, chi=64, complex128) and the % of the FP64 roofline.
 
 A *step* is one pass of the hot path over one batch: every in-flight circuit
-(one persistent slot per SM, 148 on a B200) advances by one checkpoint
+(S slots, by default two per SM = 296 on a B200, queued onto one persistent
+CTA per SM in decreasing order of predicted cost) advances by one checkpoint
 segment (10 of its 200 Trotter steps) and its <Z_j> are measured and added to
 the signed estimator sums; a slot whose circuit finished restarts with the
 next sample id (continuous batching).  20 steps = one full circuit per slot,
@@ -193,7 +194,11 @@ def run_b200(args):
     from paper_2604_13144_b200.ensemble import SlotPipeline
 
     tb, ham, cfg, pol, ck = c3_objects()
-    pipe = SlotPipeline(ham, cfg, C3["circ_seed"], "01" * (C3["n"] // 2), pol, ck, n_slots=args.slots,
+    # two slots per SM: the persistent CTAs take slots from a queue ordered by
+    # predicted segment cost, which balances the per-segment work (0.87 -> 0.985
+    # of the kernel time busy, tools/slot_balance.py)
+    sms = _lib.load().tb_num_sms(_lib.context(local))
+    pipe = SlotPipeline(ham, cfg, C3["circ_seed"], "01" * (C3["n"] // 2), pol, ck, n_slots=args.slots or 2 * sms,
                         device=local, first_sample=rank, sample_stride=world)
     S = pipe.n_slots
     plans = [pipe.plan() for _ in range(args.warmup + args.steps)]
@@ -238,7 +243,7 @@ def run_b200(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (reference-identical seeded sampler, random disorder seed 4)",
-        "config": {"workload": WORKLOAD, "slots_per_gpu": S,
+        "config": {"workload": WORKLOAD, "slots_per_gpu": S, "ctas_per_gpu": min(S, sms),
                    "step": "one checkpoint segment (10 Trotter steps) of every in-flight circuit",
                    "samples_per_step": S / 20.0, "l2": "resident MPS state %.0f MB per GPU > 126 MB L2" % (
                        S * C3["n"] * 64 * 2 * 64 * 16 / 1e6),

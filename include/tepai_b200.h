@@ -134,19 +134,23 @@ int tb_run_ensemble(tb_ctx* ctx, const tb_ensemble_desc* desc, tb_ensemble_out* 
  * NULL = legacy default) and does not synchronize unless kernel_ms != NULL. */
 int tb_run_ensemble_device(tb_ctx* ctx, const tb_ensemble_desc* desc, tb_ensemble_out* out, void* stream);
 
-/* Continuous batching ("slots"): one persistent CTA per slot keeps that
- * slot's MPS resident in HBM between calls.  Each call advances every slot
- * by its own gate-stream segment (base.gates / gate_offsets indexed by slot),
- * optionally restarting it from the product state first (reset[slot] = 1),
- * measures <Z_j> at the segment's checkpoints and adds the signed fixed-point
- * values to estimator row sum_row[slot][c].  The first call for a given
- * (n, cap, n_slots) must reset every slot; any other engine call on the same
- * context (run_stream, run_ensemble, svd) invalidates the slot states.
- * n_slots (= base.n_samples) must not exceed tb_num_sms(). */
+/* Continuous batching ("slots"): every slot keeps its MPS resident in HBM
+ * between calls.  Each call advances every slot by its own gate-stream
+ * segment (base.gates / gate_offsets indexed by slot), optionally restarting
+ * it from the product state first (reset[slot] = 1), measures <Z_j> at the
+ * segment's checkpoints and adds the signed fixed-point values to estimator
+ * row sum_row[slot][c].  The persistent CTAs (min(n_slots, tb_num_sms()))
+ * take slots from an atomic queue, in the order given by `order` (a
+ * permutation of the slots, e.g. by decreasing predicted cost; NULL = slot
+ * order), so more slots than SMs balance the per-segment work.  The first
+ * call for a given (n, cap, n_slots) must reset every slot; any other engine
+ * call on the same context (run_stream, run_ensemble, svd) invalidates the
+ * slot states. */
 typedef struct tb_step_desc {
   tb_ensemble_desc base;
   const uint8_t* reset;    /* [n_slots] */
   const int32_t* sum_row;  /* [n_slots][n_ckpt] */
+  const int32_t* order;    /* [n_slots] processing order, or NULL */
 } tb_step_desc;
 
 /* host buffers; sum_v/sum_v2 hold sum_rows x n_obs entries */

@@ -45,7 +45,8 @@ class EnsembleOut(ctypes.Structure):
 
 
 class StepDesc(ctypes.Structure):
-    _fields_ = [("base", EnsembleDesc), ("reset", ctypes.c_void_p), ("sum_row", ctypes.c_void_p)]
+    _fields_ = [("base", EnsembleDesc), ("reset", ctypes.c_void_p), ("sum_row", ctypes.c_void_p),
+                ("order", ctypes.c_void_p)]
 
 
 _lock = threading.Lock()

@@ -91,9 +91,10 @@ struct Job {
   const double2* init_mps;  // optional start MPS [n][cap][2][cap] (hybrid fan-out)
   const int32_t* init_dims; // [n+1] bond dims of init_mps
   int init_center;
-  int slot_mode;            // 0: work queue of whole samples; 1: CTA b advances slot b
+  int slot_mode;            // 0: queue of whole samples; 1: queue of slots, one segment each
   const uint8_t* reset;     // slot mode: 1 = start slot b from the product state (NULL: never)
   const int32_t* sum_row;   // [n_samples][n_ckpt] estimator row of each checkpoint (NULL: ck)
+  const int32_t* order;     // slot mode: queue position -> slot (NULL: identity)
   // outputs
   double* values;
   double* discarded;
@@ -105,9 +106,9 @@ struct Job {
   int* next_sample;
   int* status;         // bit 0: Jacobi non-convergence, bit 1: bad dims
   // run_stream mode i/o
-  int* slot_dims;        // [grid][MAXN+1] persistent slot state (slot mode)
-  int* slot_center;      // [grid]
-  double* slot_counters; // [grid][4]
+  int* slot_dims;        // [slots][MAXN+1] persistent slot state (slot mode)
+  int* slot_center;      // [slots]
+  double* slot_counters; // [slots][4]
   // workspace
   double2* ws_mps;
   double2* ws_W;
@@ -2647,16 +2648,20 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
   }
   if (job.qrcp_tmem) tmem_alloc(sm);
   for (int iter = 0;; ++iter) {
-    if (job.slot_mode) {
-      if (iter > 0 || (int)blockIdx.x >= job.n_samples) break;
-      if (threadIdx.x == 0) sm.sample = blockIdx.x;
-    } else if (threadIdx.x == 0) {
-      sm.sample = atomicAdd(job.next_sample, 1);
+    // both modes take work items from an atomic queue: whole samples (queue
+    // mode) or slots, each advanced by one checkpoint segment (slot mode).
+    // More slots than CTAs balance the per-segment work (a segment's cost
+    // varies with its ring-gate count) instead of waiting for the slowest.
+    if (threadIdx.x == 0) {
+      const int q = atomicAdd(job.next_sample, 1);
+      sm.sample = (q < job.n_samples && job.slot_mode && job.order) ? job.order[q] : q;
     }
     __syncthreads();
     const int sample = sm.sample;
     if (sample >= job.n_samples) break;
-    int* sdims = job.slot_dims + (size_t)blockIdx.x * (MAXN + 1);
+    // a slot's MPS and bookkeeping live with the slot, not with the CTA
+    if (job.slot_mode) cx.mps = job.ws_mps + job.mps_stride * (size_t)sample;
+    int* sdims = job.slot_dims + (size_t)sample * (MAXN + 1);
     // --- initial state: product state, or the slot's persistent state
     const bool fresh = !job.slot_mode || (job.reset && job.reset[sample]);
     if (fresh && job.init_mps) {
@@ -2693,8 +2698,8 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
     } else {
       for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = sdims[e];
       if (threadIdx.x == 0) {
-        sm.center = job.slot_center[blockIdx.x];
-        for (int q = 0; q < 4; ++q) sm.counters[q] = job.slot_counters[(size_t)blockIdx.x * 4 + q];
+        sm.center = job.slot_center[sample];
+        for (int q = 0; q < 4; ++q) sm.counters[q] = job.slot_counters[(size_t)sample * 4 + q];
       }
     }
     __syncthreads();
@@ -2751,8 +2756,8 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
       if (job.ledger)
         for (int q = 0; q < 4; ++q) job.ledger[(size_t)sample * 4 + q] = sm.counters[q];
       if (job.slot_mode) {
-        job.slot_center[blockIdx.x] = sm.center;
-        for (int q = 0; q < 4; ++q) job.slot_counters[(size_t)blockIdx.x * 4 + q] = sm.counters[q];
+        job.slot_center[sample] = sm.center;
+        for (int q = 0; q < 4; ++q) job.slot_counters[(size_t)sample * 4 + q] = sm.counters[q];
       }
     }
     if (job.slot_mode)
@@ -3373,7 +3378,6 @@ int tb_step_device(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, void* 
   int rc = validate_desc(c, d, o);
   if (rc) return rc;
   if (d->n_samples == 0) return TB_OK;
-  if (d->n_samples > c->sms) return fail(c, TB_EINVAL, "more slots than SMs (one persistent CTA per slot)");
   if (!sd->reset || (d->n_ckpt > 0 && !sd->sum_row)) return fail(c, TB_EINVAL, "null reset/sum_row");
   rc = ensure_workspace(c, d->n_samples, d->n, d->cap);
   if (rc) return rc;
@@ -3386,7 +3390,9 @@ int tb_step_device(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, void* 
   job.slot_mode = 1;
   job.reset = sd->reset;
   job.sum_row = sd->sum_row;
-  return launch(c, job, d->n_samples, (cudaStream_t)stream, o->flops, o->kernel_ms);
+  job.order = sd->order;
+  const int grid = d->n_samples < c->sms ? d->n_samples : c->sms;
+  return launch(c, job, grid, (cudaStream_t)stream, o->flops, o->kernel_ms);
 }
 
 int tb_step(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, int64_t sum_rows) {
@@ -3403,6 +3409,8 @@ int tb_step(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, int64_t sum_r
   if ((rc = stage_inputs(c, sg, d, &sdd.base)) || (rc = stage_outputs(c, sg, d, o, &od))) return rc;
   sdd.reset = sg.up(sd->reset, (size_t)d->n_samples);
   sdd.sum_row = sg.up(sd->sum_row, (size_t)d->n_samples * d->n_ckpt);
+  sdd.order = sd->order ? sg.up(sd->order, (size_t)d->n_samples) : nullptr;
+  if (sd->order && !sdd.order) return fail(c, TB_ENOMEM, "device allocation failed");
   od.sum_v = sg.up(o->sum_v, (size_t)sum_rows * d->n_obs);
   od.sum_v2 = sg.up(o->sum_v2, (size_t)sum_rows * d->n_obs);
   if (!sdd.reset || !sdd.sum_row || !od.sum_v || !od.sum_v2) return fail(c, TB_ENOMEM, "device allocation failed");

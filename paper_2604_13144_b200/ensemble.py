@@ -245,6 +245,22 @@ def allreduce_sums(run: EnsembleRun, group=None) -> EnsembleRun:
                        run.wall_s, dict(run.extra))
 
 
+def slot_order(words: np.ndarray, offsets: np.ndarray) -> np.ndarray:
+    """Slot processing order for one step: decreasing predicted cost, so the
+    persistent CTAs' atomic slot queue approximates longest-processing-time
+    scheduling.  The cost of a segment is its number of two-site SVD updates:
+    1 per adjacent two-site gate and 2 (b - a - 1) + 1 per non-adjacent (ring)
+    gate, whose swap sweep costs one update per swap (_kernel.py:203-215)."""
+    a = (words & 0xFF).astype(np.int64)
+    b = ((words >> 8) & 0xFF).astype(np.int64)
+    cost = np.where(b == 0xFF, 0, np.where(b - a > 1, 2 * (b - a - 1) + 1, 1))
+    if words.size == 0:
+        return np.arange(offsets.size - 1, dtype=np.int32)
+    seg = np.add.reduceat(cost, np.minimum(offsets[:-1], words.size - 1))
+    seg = np.where(np.diff(offsets) > 0, seg, 0)  # reduceat returns an element for empty segments
+    return np.argsort(-seg, kind="stable").astype(np.int32)
+
+
 @dataclass
 class StepPlan:
     """Host inputs of one pipeline step (one checkpoint segment per slot)."""
@@ -256,6 +272,7 @@ class StepPlan:
     reset: np.ndarray      # uint8 [S]
     sum_row: np.ndarray    # int32 [S, 1]
     completes: int         # samples finished by this step
+    order: np.ndarray | None = None  # int32 [S] slot processing order (decreasing predicted cost)
 
 
 class SlotPipeline:
@@ -279,7 +296,7 @@ class SlotPipeline:
                                    init_state)
         ctx = _lib.context(device)
         sms = _lib.load().tb_num_sms(ctx)
-        self.n_slots = min(n_slots or sms, sms)
+        self.n_slots = int(n_slots or sms)  # > sms: slots queue onto the persistent CTAs
         self.table = TermTable.of(ham)
         self.next_id = first_sample
         self.stride = sample_stride
@@ -321,7 +338,8 @@ class SlotPipeline:
         offs = np.zeros(S + 1, np.int64)
         offs[1:] = np.cumsum([s.size for s in segs])
         ends = np.diff(offs).astype(np.int32).reshape(S, 1)
-        return StepPlan(np.concatenate(segs).astype(np.uint32), offs, ends, sign, reset, row, completes)
+        words = np.concatenate(segs).astype(np.uint32)
+        return StepPlan(words, offs, ends, sign, reset, row, completes, slot_order(words, offs))
 
     def _desc(self, ptrs, S):
         p = self.proto
@@ -329,7 +347,7 @@ class SlotPipeline:
                                  p.angle_cs.shape[0], ptrs["words"], ptrs["offsets"], ptrs["ckpt_end"],
                                  ptrs["ckpt_sign"], ptrs["angle_cs"], None, ptrs["obs"], ptrs["init"],
                                  ptrs.get("init_mps"), ptrs.get("init_dims"), p.init_center, 0)
-        return _lib.StepDesc(base, ptrs["reset"], ptrs["sum_row"])
+        return _lib.StepDesc(base, ptrs["reset"], ptrs["sum_row"], ptrs.get("order"))
 
     def step_host(self, plan: StepPlan, values: np.ndarray | None = None) -> float:
         """End-to-end step through ``tb_step`` with host buffers; returns kernel ms."""
@@ -339,6 +357,9 @@ class SlotPipeline:
         keep = [np.ascontiguousarray(x) for x in keep]
         ptrs = dict(zip(["words", "offsets", "ckpt_end", "ckpt_sign", "reset", "sum_row", "angle_cs", "obs", "init"],
                         [x.ctypes.data for x in keep]))
+        if plan.order is not None:
+            keep.append(np.ascontiguousarray(plan.order, dtype=np.int32))
+            ptrs["order"] = keep[-1].ctypes.data
         if self.proto.init_mps is not None:
             ptrs["init_mps"] = self.proto.init_mps.ctypes.data
             ptrs["init_dims"] = self.proto.init_dims.ctypes.data
@@ -362,6 +383,8 @@ class SlotPipeline:
         t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in (
             ("words", plan.words.view(np.int32)), ("offsets", plan.offsets), ("ckpt_end", plan.ckpt_end),
             ("ckpt_sign", plan.ckpt_sign), ("reset", plan.reset), ("sum_row", plan.sum_row))}
+        if plan.order is not None:
+            t["order"] = torch.from_numpy(np.ascontiguousarray(plan.order, dtype=np.int32)).to(dev)
         t["completes"] = plan.completes
         return t
 
@@ -387,6 +410,8 @@ class SlotPipeline:
         """Device-resident step through ``tb_step_device`` on ``stream_ptr``."""
         S = self.n_slots
         ptrs = {k: t[k].data_ptr() for k in ("words", "offsets", "ckpt_end", "ckpt_sign", "reset", "sum_row")}
+        if "order" in t:
+            ptrs["order"] = t["order"].data_ptr()
         ptrs.update(angle_cs=ds["angle_cs"].data_ptr(), obs=ds["obs"].data_ptr(), init=ds["init"].data_ptr())
         if "init_mps" in ds:
             ptrs.update(init_mps=ds["init_mps"].data_ptr(), init_dims=ds["init_dims"].data_ptr())

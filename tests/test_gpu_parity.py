@@ -279,28 +279,31 @@ def test_empty_and_degenerate_inputs(engine):
     assert run.n_samples == 0
 
 
-def test_slot_pipeline_matches_whole_circuit_runs(engine, golden):
+@pytest.mark.parametrize("slots", [12, 300])
+def test_slot_pipeline_matches_whole_circuit_runs(engine, golden, slots):
     """Continuous batching (tb_step, one checkpoint segment per launch, slots
     restarted with new sample ids) gives the same estimator sums as
-    tb_run_ensemble over the same ids (bench.py's step definition)."""
+    tb_run_ensemble over the same ids (bench.py's step definition); 300 slots
+    exceed the SM count, so slots queue onto the persistent CTAs and a slot's
+    state moves between CTAs from one launch to the next."""
     ref = golden("ref_c1.npz")
     ham = tb.build_spin_ring(8, 1.0, 0)
     cfg = tb.PaiConfig(DELTA, 100, 1.0)
     ck = ref["checkpoints"]
-    pipe = tb.SlotPipeline(ham, cfg, 1, "01" * 4, tb.TruncationPolicy(16), ck, n_slots=12, pi_local=False)
+    pipe = tb.SlotPipeline(ham, cfg, 1, "01" * 4, tb.TruncationPolicy(16), ck, n_slots=slots, pi_local=False)
     per_sample = {}
-    for _ in range(2 * ck.size):  # two full circuits per slot: ids 0..23
+    for _ in range(2 * ck.size):  # two full circuits per slot: ids 0 .. 2 slots - 1
         plan = pipe.plan()
         vals = np.zeros((pipe.n_slots, 1, 8))
         ids = [pipe.slot_pack[b] for b in range(pipe.n_slots)]
         pipe.step_host(plan, vals)
         for b in range(pipe.n_slots):
             per_sample.setdefault(id(ids[b]), []).append(vals[b, 0])
-    assert pipe.completed == 24
-    run = tb.run_ensemble(ham, cfg, 1, range(24), "01" * 4, tb.TruncationPolicy(16), ck, pi_local=False)
+    assert pipe.completed == 2 * slots
+    run = tb.run_ensemble(ham, cfg, 1, range(2 * slots), "01" * 4, tb.TruncationPolicy(16), ck, pi_local=False)
     np.testing.assert_array_equal(pipe.sum_v, run.sum_v)
     np.testing.assert_array_equal(pipe.sum_v2, run.sum_v2)
-    np.testing.assert_array_equal(pipe.row_count, np.full(ck.size, 24))
+    np.testing.assert_array_equal(pipe.row_count, np.full(ck.size, 2 * slots))
     st = pipe.stats()
     np.testing.assert_allclose(st[ck.size - 1]["estimate"], run.stats()["estimate"][-1], atol=1e-15)
 

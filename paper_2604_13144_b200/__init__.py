@@ -35,7 +35,7 @@ from .mps import (
     snapshot_from_bytes,
     snapshot_to_bytes,
 )
-from .pauli import Hamiltonian, HamTerm, PauliString, build_spin_ring, coeff_l1_norm
+from .pauli import Hamiltonian, HamTerm, PauliString, build_spin_ring, build_tfim_ring, coeff_l1_norm, min_trotter_steps
 from .rng import circuit_stream, disorder_stream, philox_stream
 from .sampling import (
     PaiConfig,

@@ -156,3 +156,47 @@ def build_spin_ring(n: int, coupling: float, omega: Sequence[float] | int) -> Ha
 def coeff_l1_norm(ham: Hamiltonian) -> float:
     """Sum of |c_k| (ref pauli.py:210-212)."""
     return float(sum(abs(t.coeff) for t in ham.terms))
+
+
+def build_tfim_ring(n: int, field: float, seed: int, j_range=(0.5, 1.5), h_range=(-1.0, 1.0)) -> Hamiltonian:
+    """Periodic disordered transverse-field Ising ring (BASELINE config 4):
+    H = sum_j J_j Z_j Z_{j+1} + g sum_j X_j + sum_j h_j Z_j.
+
+    The reference ships only the generic ``Hamiltonian``/``HamTerm`` types
+    (ref pauli.py:130-167) and no TFIM builder, so this module fixes the two
+    conventions the config leaves open, mirroring ``build_spin_ring``
+    (ref pauli.py:170-207):
+    - draw order: ``J = U[j_range]`` for bonds 0..n-1, then ``h = U[h_range]``
+      for sites 0..n-1, both from ``disorder_stream(seed)``;
+    - term order: the Z fields h_k Z_k by site, then the X fields g X_k by site,
+      then the couplings J_b Z_b Z_{b+1} by bond, the wrap bond stored sorted
+      as Z_0 Z_{n-1} (the only non-adjacent pair).
+    Zero coefficients are dropped as in the reference builder.
+    """
+    if n < 3:
+        raise ValueError(f"ring needs n >= 3, got {n}")
+    if not math.isfinite(field):
+        raise ValueError("non-finite transverse field")
+    rng = disorder_stream(int(seed))
+    couplings = rng.uniform(j_range[0], j_range[1], size=n)
+    fields = rng.uniform(h_range[0], h_range[1], size=n)
+    terms = [HamTerm(float(fields[k]), PauliString.single(n, k, "Z")) for k in range(n) if fields[k] != 0.0]
+    if field != 0.0:
+        terms.extend(HamTerm(float(field), PauliString.single(n, k, "X")) for k in range(n))
+    for b in range(n):
+        if couplings[b] != 0.0:
+            pair = (b, (b + 1) % n)
+            terms.append(HamTerm(float(couplings[b]), PauliString(n, tuple((q, "Z") for q in pair))))
+    return Hamiltonian(n, tuple(terms), coupling=0.0, seed=int(seed))
+
+
+def min_trotter_steps(ham: Hamiltonian, delta: float, total_time: float) -> int:
+    """Smallest step count N with max_k |2 c_k T / N| <= delta, i.e. the first
+    N that ``PaiConfig.validate_against`` (ref sampling.py:64-84) accepts."""
+    cmax = max(abs(t.coeff) for t in ham.terms)
+    steps = max(1, math.ceil(2.0 * cmax * total_time / delta))
+    while 2.0 * cmax * total_time / steps > delta * (1.0 + 1e-12):
+        steps += 1
+    while steps > 1 and 2.0 * cmax * total_time / (steps - 1) <= delta * (1.0 + 1e-12):
+        steps -= 1
+    return steps

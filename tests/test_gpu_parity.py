@@ -345,3 +345,30 @@ def test_hybrid_trotter_then_tepai_vs_reference(engine, golden):
     signs = ref["sign"].astype(np.float64)
     want = tb.estimator.quantize(signs[:, :, None] * ref["vals"]).sum(axis=0)
     assert np.max(np.abs(run.sum_v - want)) <= 16  # 2^-40 quantisation of values equal to 1e-10
+
+
+def test_tfim_ensemble_and_trotter_vs_reference(engine, golden):
+    """Config 4 physics at desk scale (tests/golden/make_golden_tfim.py): the
+    transverse-field Ising ring has non-diagonal X-field one-site gates and
+    Z_bZ_{b+1} couplings; 16 TE-PAI samples from |000000> untruncated, and the
+    deterministic Trotter circuit on the same kernels at chi 8 (exact) and
+    chi 4 (truncation active, discarded weight ~1.7e-8)."""
+    ref = golden("ref_tfim_n6.npz")
+    ham = tb.build_tfim_ring(6, 1.0, 6)
+    np.testing.assert_array_equal(ham.coefficients(), ref["coeffs"])
+    cfg = tb.PaiConfig(math.pi / 2**6, 40, 0.5)
+    ck = [int(j) for j in ref["checkpoints"]]
+    run = tb.run_ensemble(ham, cfg, 7, range(16), "0" * 6, tb.TruncationPolicy(8, 1e-12), ck, pi_local=False)
+    np.testing.assert_allclose(run.values, ref["vals"], atol=1e-10)
+    run_pi = tb.run_ensemble(ham, cfg, 7, range(16), "0" * 6, tb.TruncationPolicy(8, 1e-12), ck, pi_local=True)
+    np.testing.assert_allclose(run_pi.values, ref["vals"], atol=1e-10)
+    for chi, key, tol in ((8, "trot_exact", 1e-10), (4, "trot_trunc", 1e-8)):
+        st, done, out = tb.init_product_state("0" * 6), 0, []
+        for j in ck:
+            tb.run_circuit(st, tb.build_trotter_circuit(ham, (j - done) * 0.5 / 40, j - done),
+                           tb.TruncationPolicy(chi, 1e-12))
+            done = j
+            out.append([tb.expectation(st, tb.PauliString.single(6, q, "Z")) for q in range(6)])
+        np.testing.assert_allclose(np.array(out), ref[key], atol=tol)
+    if chi == 4:
+        assert st.discarded_weight == pytest.approx(float(ref["trot_trunc_discarded"]), rel=1e-6)

@@ -79,3 +79,48 @@ def test_oracle_pi_local_equals_full_update_untruncated():
     b.run(ops, None, 1e-14, pi_local=True)
     np.testing.assert_allclose(a.z_profile(), b.z_profile(), atol=1e-12)
     assert abs(abs(np.vdot(_psi(a), _psi(b))) - 1.0) < 1e-12
+
+
+def _tfim_setup(ref):
+    ham = tb.build_tfim_ring(6, 1.0, 6)
+    np.testing.assert_array_equal(ham.coefficients(), ref["coeffs"])  # same draw and term order as the fixture
+    return ham, tb.PaiConfig(math.pi / 2**6, 40, 0.5)
+
+
+def test_tfim_builder_conventions():
+    ham = tb.build_tfim_ring(8, 1.0, 6)
+    labels = [t.pauli.label() for t in ham.terms]
+    assert labels[:8] == [tb.PauliString.single(8, k, "Z").label() for k in range(8)]
+    assert labels[8:16] == [tb.PauliString.single(8, k, "X").label() for k in range(8)]
+    assert [t.pauli.support for t in ham.terms[16:]] == [(b, b + 1) for b in range(7)] + [(0, 7)]
+    assert all(0.5 <= t.coeff <= 1.5 for t in ham.terms[16:])
+    # config 4 as written is outside the sampler's domain; the first feasible step count is accepted
+    big = tb.build_tfim_ring(50, 1.0, 6)
+    with pytest.raises(ValueError):
+        tb.PaiConfig(math.pi / 2**8, 300, 3.0).validate_against(big)
+    n = tb.min_trotter_steps(big, math.pi / 2**8, 3.0)
+    tb.PaiConfig(math.pi / 2**8, n, 3.0).validate_against(big)
+    with pytest.raises(ValueError):
+        tb.PaiConfig(math.pi / 2**8, n - 1, 3.0).validate_against(big)
+
+
+@pytest.mark.parametrize("i", [0, 5, 11])
+def test_oracle_tfim_matches_reference(golden, i):
+    ref = golden("ref_tfim_n6.npz")
+    ham, cfg = _tfim_setup(ref)
+    circ = tb.sample_circuit(ham, cfg, tb.circuit_stream(7, i), sample_id=i)
+    vals, sign, _, _ = run_sample_checkpoints(circ, "0" * 6, 8, 1e-12, list(ref["checkpoints"]))
+    np.testing.assert_allclose(vals, ref["vals"][i], atol=1e-12)
+    np.testing.assert_array_equal(sign, ref["sign"][i])
+
+
+def test_oracle_tfim_trotter_matches_reference(golden):
+    ref = golden("ref_tfim_n6.npz")
+    ham, _ = _tfim_setup(ref)
+    for chi, key in ((8, "trot_exact"), (4, "trot_trunc")):
+        st, done, out = OracleMPS("0" * 6), 0, []
+        for j in ref["checkpoints"]:
+            st.run(tb.build_trotter_circuit(ham, (j - done) * 0.5 / 40, int(j - done)).operations(), chi, 1e-12)
+            done = j
+            out.append(st.z_profile())
+        np.testing.assert_allclose(np.array(out), ref[key], atol=1e-12)

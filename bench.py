@@ -8,18 +8,26 @@ segment (10 of its 200 Trotter steps) and its <Z_j> are measured and added to
 the signed estimator sums; a slot whose circuit finished restarts with the
 next sample id (continuous batching).  20 steps = one full circuit per slot,
 so samples/s = slots * K / 20 / T (sample-equivalents).  All slots start at
-step 0, so the default window (W=3, K=17) is segments 3..19 of the first
-circuits — it omits the cheap bond-growth segments and therefore
-under-states the throughput of complete circuits.
+step 0; the default window (W=3, K=20, as the driver's W=5, K=20) times
+exactly one full lifecycle per slot — every segment index 0..19 once,
+segments 3..19 of the first circuits and 0..2 of the next.
 
 ``value`` uses the device time of the K persistent-kernel launches (inputs
 already in HBM when each launch starts); ``e2e`` is the wall time of the same
-K steps through the host-buffer C ABI call ``tb_step`` (H2D of the step's gate
-words, D2H of <Z_j> and sums, inside the timed region).
+K steps through the host-buffer C ABI call ``tb_step``: the host producer
+thread (reference-identical sampler + packing, running ahead of the engine),
+H2D of the step's gate words, the kernel, D2H of <Z_j>, the sums and the
+per-slot exclusion flags, and the final reduction of the estimator sums.
 
-``--impl reference`` times the CPU path instead: the numpy port of the
-reference engine (oracle/, same LAPACK calls), one process per host core,
-each advancing its own circuit by one segment per step.
+``cpu_baseline`` (rank 0, N=1) times the numpy port of the reference engine
+(oracle/, pinned bit-identical to the un-jitted reference) on every host core:
+one circuit per core through one full 20-segment lifecycle, free-running.
+
+``--impl reference`` is the reference arm: the same port on every host core
+over the same W + K segment window, timed free-running (last end - first
+start, no per-step barriers), plus — when the unmodified reference is
+installed under baseline/_ref — that package itself (NUMBA_DISABLE_JIT=1)
+over the first half of the lifecycle as a second CPU figure.
 """
 
 from __future__ import annotations
@@ -106,43 +114,85 @@ def c3_objects():
 
 
 # ---------------------------------------------------------------------------
-# CPU arm: numpy port of the reference engine (oracle/), one process per core
+# CPU arm: the reference engine's CPU path, one process per host core
 # ---------------------------------------------------------------------------
+REF_SITE = os.path.join(ROOT, "baseline", "_ref")  # unmodified reference (pip --target, git-ignored)
+
+
 def _cpu_worker(args):
+    """Advance circuit `sid` by n_segments checkpoint segments (restarting at
+    each lifecycle end) and return the monotonic (start, end) of every segment.
+    engine "port": the numpy restatement in oracle/ (pinned bit-identical to
+    the un-jitted reference); "reference": the unmodified reference package
+    from baseline/_ref with NUMBA_DISABLE_JIT=1 (its numba kernel does not
+    compile under numba 0.65)."""
+    sid, n_segments, engine = args
     from threadpoolctl import threadpool_limits
 
     threadpool_limits(1)
-    sid, n_segments, conn = args
     tb, ham, cfg, pol, ck = c3_objects()
-    from oracle.mps_oracle import OracleMPS
-
     circ = tb.sample_circuit(ham, cfg, tb.circuit_stream(C3["circ_seed"], sid), sample_id=sid)
-    st = OracleMPS("01" * (C3["n"] // 2))
-    times, lo = [], 0
+    labels = "01" * (C3["n"] // 2)
+    if engine == "reference":
+        os.environ["NUMBA_DISABLE_JIT"] = "1"
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+        sys.path.insert(0, REF_SITE)
+        import dataclasses
+
+        import tepai
+
+        zs = [tepai.PauliString.single(C3["n"], q, "Z") for q in range(C3["n"])]
+        rc = tepai.sample_circuit(tepai.build_spin_ring(C3["n"], 1.0, C3["ham_seed"]),
+                                  tepai.PaiConfig(math.pi / 2**7, C3["n_steps"], C3["total_time"]),
+                                  tepai.rng.circuit_stream(C3["circ_seed"], sid), sample_id=sid)
+        policy = tepai.TruncationPolicy(chi_cut=C3["chi"], svalue_floor=1e-12)
+
+        def fresh():
+            return tepai.init_product_state(labels)
+
+        def advance(st, lo, hi):
+            seg = dataclasses.replace(rc, term_index=rc.term_index[lo:hi], step_index=rc.step_index[lo:hi],
+                                      kinds=rc.kinds[lo:hi], signs=rc.signs[lo:hi])
+            tepai.run_circuit(st, seg, policy)
+            return [tepai.expectation(st, z) for z in zs]
+    else:
+        from oracle.mps_oracle import OracleMPS
+
+        def fresh():
+            return OracleMPS(labels)
+
+        def advance(st, lo, hi):
+            st.run(circ.slice_entries(lo, hi).operations(), C3["chi"], 1e-12)
+            return [st.expect({j: "Z"}) for j in range(C3["n"])]
+    st, lo, stamps = None, 0, []
     for c in range(n_segments):
-        hi = int(np.searchsorted(circ.step_index, ck[c % ck.size]))
         if c % ck.size == 0:
-            st, lo = OracleMPS("01" * (C3["n"] // 2)), 0
-        t0 = time.perf_counter()
-        st.run(circ.slice_entries(lo, hi).operations(), C3["chi"], 1e-12)
-        _ = [st.expect({j: "Z"}) for j in range(C3["n"])]
-        times.append(time.perf_counter() - t0)
+            st, lo = fresh(), 0
+        hi = int(np.searchsorted(circ.step_index, ck[c % ck.size]))
+        t0 = time.monotonic()
+        advance(st, lo, hi)
+        stamps.append((t0, time.monotonic()))
         lo = hi
-    return times
+    return stamps
 
 
-def cpu_segments(n_segments: int, cores: int):
-    """Each of `cores` processes advances its own circuit by n_segments
-    checkpoint segments; returns the per-step wall times (max over cores)."""
+def cpu_run(n_segments: int, cores: int, engine: str = "port"):
+    """`cores` free-running processes, each advancing its own circuit (ids
+    0..cores-1) by n_segments segments; returns stamps[core][segment] =
+    (start, end) on the shared monotonic clock."""
     import multiprocessing as mp
 
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, [(i, n_segments, None) for i in range(cores)])
-        wall = time.perf_counter() - t0
-    per_step = np.max(np.array(res), axis=0)
-    return per_step, wall
+        return np.array(pool.map(_cpu_worker, [(i, n_segments, engine) for i in range(cores)]))
+
+
+def cpu_rate(stamps: np.ndarray, first: int, count: int):
+    """Free-running throughput over segments [first, first + count): every
+    core's work in that window / (last end - first start), no per-step
+    barriers.  Returns (samples/s, wall seconds)."""
+    wall = float(stamps[:, first + count - 1, 1].max() - stamps[:, first, 0].min())
+    return stamps.shape[0] * count / 20.0 / wall, wall
 
 
 def host_cores():
@@ -152,26 +202,49 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
     cores = host_cores()
     steps = args.warmup + args.steps
-    per_step, wall = cpu_segments(steps, cores)
-    timed = float(np.sum(per_step[args.warmup:]))
-    value = cores * args.steps / 20.0 / timed
+    stamps = cpu_run(steps, cores, "port")
+    value, wall = cpu_rate(stamps, args.warmup, args.steps)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * timed / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (reference sampler, seeded)",
         "config": {"workload": WORKLOAD, "step": "one checkpoint segment (10 Trotter steps) per in-flight circuit",
                    "slots": cores, "parallelism": f"{cores} CPU processes"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{cores} circuits x {steps} checkpoint segments (numpy port of the reference "
-                                   f"engine, zgesdd via numpy LAPACK, 1 thread per process)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"{cores} free-running processes, circuits 0..{cores - 1}, segments {args.warmup}.."
+                                   f"{steps - 1} of the lifecycle timed (numpy port of the reference engine, zgesdd "
+                                   f"via numpy LAPACK, 1 thread per process); wall = last end - first start"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_unmodified and os.path.isdir(os.path.join(REF_SITE, "tepai")):
+        # second CPU figure: the unmodified reference itself, un-jitted, on the
+        # same cores over the first half of the lifecycle, next to the port on
+        # the same window (the port's arithmetic is the reference's)
+        seg = args.unmodified_segments
+        ref = cpu_run(seg, cores, "reference")
+        rv, rw = cpu_rate(ref, 0, seg)
+        pv, pw = cpu_rate(stamps, 0, min(seg, steps))
+        line["reference_unmodified"] = {
+            "value": rv, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "wall_s": rw,
+            "sample": f"{cores} circuits x segments 0..{seg - 1} (bond-growth half of the lifecycle), unmodified "
+                      "reference package (baseline/_ref, NUMBA_DISABLE_JIT=1)",
+            "port_same_window": pv}
     print(json.dumps(line), flush=True)
 
 
@@ -191,36 +264,38 @@ def run_b200(args):
 
     __graft_entry__.build()
     from paper_2604_13144_b200 import _lib
-    from paper_2604_13144_b200.ensemble import SlotPipeline
+    from paper_2604_13144_b200.ensemble import pipeline_shard, reduce_pipeline
 
     tb, ham, cfg, pol, ck = c3_objects()
     # two slots per SM: the persistent CTAs take slots from a queue ordered by
     # predicted segment cost, which balances the per-segment work (0.87 -> 0.985
     # of the kernel time busy, tools/slot_balance.py)
     sms = _lib.load().tb_num_sms(_lib.context(local))
-    pipe = SlotPipeline(ham, cfg, C3["circ_seed"], "01" * (C3["n"] // 2), pol, ck, n_slots=args.slots or 2 * sms,
-                        device=local, first_sample=rank, sample_stride=world)
+    pipe = pipeline_shard(ham, cfg, C3["circ_seed"], "01" * (C3["n"] // 2), pol, ck, n_slots=args.slots or 2 * sms,
+                          rank=rank, world=world, device=local)
     S = pipe.n_slots
-    plans = [pipe.plan() for _ in range(args.warmup + args.steps)]
-    h2d = [sum(x.nbytes for x in (p.words, p.offsets, p.ckpt_end, p.ckpt_sign, p.reset, p.sum_row)) for p in plans]
-    d2h = S * C3["n"] * 8 + 2 * pipe.sum_v.nbytes
-    for i, p in enumerate(plans[: args.warmup]):
-        ms = pipe.step_host(p)
+    # the host producer (reference sampler + packing) runs ahead in a thread for
+    # every step, warm-up and timed alike: its work overlaps the engine calls,
+    # and whatever it does not hide lands inside the e2e wall time
+    plans = pipe.planned(args.warmup + args.steps)
+    for i in range(args.warmup):
+        ms = pipe.step_host(next(plans))
         print(f"[bench] warmup step {i}: {ms:.0f} ms", file=sys.stderr, flush=True)
+    d2h = S * C3["n"] * 8 + 2 * pipe.sum_v.nbytes + S * 4
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    kernel_ms, flops0 = [], pipe.flops
+    kernel_ms, h2d, flops0 = [], [], pipe.flops
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for i, p in enumerate(plans[args.warmup:]):
+        for i in range(args.steps):
+            p = next(plans)
+            h2d.append(p.nbytes())
             kernel_ms.append(pipe.step_host(p))
             print(f"[bench] step {i}: {kernel_ms[-1]:.0f} ms", file=sys.stderr, flush=True)
         torch.cuda.synchronize()
-        if world > 1:
-            sums = torch.from_numpy(np.concatenate([pipe.sum_v.ravel(), pipe.sum_v2.ravel()])).cuda()
-            dist.all_reduce(sums)  # the path's only collective: estimator sums
+        run = reduce_pipeline(pipe)  # the path's only collective: the estimator sums
         wall = time.perf_counter() - t0
     dev_s = sum(kernel_ms) / 1e3
     flops = pipe.flops - flops0
@@ -247,23 +322,25 @@ def run_b200(args):
                    "step": "one checkpoint segment (10 Trotter steps) of every in-flight circuit",
                    "samples_per_step": S / 20.0, "l2": "resident MPS state %.0f MB per GPU > 126 MB L2" % (
                        S * C3["n"] * 64 * 2 * 64 * 16 / 1e6),
-                   "parallelism": f"dp{world} (sample sharding, one NCCL all_reduce of the estimator sums)"},
+                   "parallelism": f"dp{world} (sample sharding, one all_reduce of the estimator sums)",
+                   "samples_completed": int(run.n_samples)},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "peak_source": "measured FP64 DMMA rate (MEASURED_PEAKS.json has no FP64 entry)",
                      "flops": "SURVEY.md §8(d) algorithmic count (two-site contraction + LAPACK-nominal SVD + QR moves)"},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(np.mean(h2d[args.warmup:])),
-                "d2h_bytes_per_step": int(d2h)},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(np.mean(h2d)), "d2h_bytes_per_step": int(d2h),
+                "includes": "host sampling + packing (producer thread), H2D, kernel, D2H, final all_reduce"},
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = host_cores()
-        per_step, _ = cpu_segments(args.cpu_segments, cores)
-        cpu = cores * args.cpu_segments / 20.0 / float(np.sum(per_step))
-        line["cpu_baseline"] = {"value": cpu, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"{cores} circuits x first {args.cpu_segments} checkpoint segments (cheap "
-                                          "bond-growth phase, so this over-states the CPU rate)"}
+        stamps = cpu_run(20, cores, "port")
+        cpu, cwall = cpu_rate(stamps, 0, 20)
+        line["cpu_baseline"] = {"value": cpu, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+                                "sample": f"{cores} circuits x one full 20-segment lifecycle, free-running processes "
+                                          f"({cwall:.0f} s wall; numpy port of the reference engine, 1 thread each)"}
+    pipe.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -273,12 +350,13 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=17)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--slots", type=int, default=None)
-    ap.add_argument("--cpu-segments", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-unmodified", action="store_true", help="reference arm: skip the unmodified-reference figure")
+    ap.add_argument("--unmodified-segments", type=int, default=10)
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

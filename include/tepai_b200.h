@@ -54,7 +54,13 @@ void tb_destroy(tb_ctx* ctx);
 const char* tb_last_error(const tb_ctx* ctx);
 /* Number of SMs of the bound device (persistent-grid size). */
 int tb_num_sms(const tb_ctx* ctx);
-/* Diagnostics: clock64 phase counters of the last ensemble launch, summed over
+/* Read and clear the context's sticky device status word (device-buffer
+ * calls do not synchronize, so they report through it): bit 0 = a Jacobi SVD
+ * did not converge, bit 2 = a slot was continued (reset = 0) although its
+ * state belongs to an older workspace generation. */
+int tb_take_status(tb_ctx* ctx, int32_t* status);
+/* Diagnostics (collected only when the context was created with TB_PROFILE=1
+ * in the environment): clock64 phase counters of the last ensemble launch, summed over
  * CTAs: [0] Jacobi cycles [1] Jacobi calls [2] sweeps [3] centre moves
  * [4] contraction+gate [5] sort+split write-back [6] <Z> sweeps
  * [7] per-sample totals [9..11] cycles/calls/sweeps of 128x128 problems,
@@ -123,6 +129,16 @@ typedef struct tb_ensemble_out {
   int64_t* sum_v2;    /* [n_ckpt][n_obs] += round(2^40 * <Z>^2) (accumulated) */
   double* flops;      /* [1] += algorithmic FLOPs (SURVEY.md §8(d) count) */
   float* kernel_ms;   /* [1] device time of the persistent kernel (CUDA events) */
+  /* [n_samples] per-sample failure report, or NULL.  A sample whose circuit
+   * hits a Jacobi SVD that does not converge (the reference would raise
+   * LinAlgError from LAPACK, _kernel.py:117) keeps its raw values, but its
+   * checkpoints from that one on are left out of sum_v / sum_v2; excluded[s]
+   * is the first such checkpoint, -1 when every checkpoint contributed.  With
+   * this array the launch succeeds and the caller drops those rows from its
+   * counts; without it the call returns TB_ENOCONV and (host-buffer calls)
+   * leaves every caller array untouched.  Device calls: the caller fills it
+   * with -1 before the launch. */
+  int32_t* excluded;
 } tb_ensemble_out;
 
 /* Host-buffer ensemble run: uploads the streams, runs the persistent kernel,
@@ -145,7 +161,10 @@ int tb_run_ensemble_device(tb_ctx* ctx, const tb_ensemble_desc* desc, tb_ensembl
  * order), so more slots than SMs balance the per-segment work.  The first
  * call for a given (n, cap, n_slots) must reset every slot; any other engine
  * call on the same context (run_stream, run_ensemble, svd) invalidates the
- * slot states. */
+ * slot states.  This is enforced: every slot state carries the workspace
+ * generation it was built in, and continuing a slot of an older generation
+ * fails the call with TB_EINVAL (status bit 2) instead of reading stale
+ * memory.  Give each pipeline its own context to keep the pools apart. */
 typedef struct tb_step_desc {
   tb_ensemble_desc base;
   const uint8_t* reset;    /* [n_slots] */

@@ -18,6 +18,8 @@ from .ensemble import (
     run_ensemble,
     run_packed,
     shard_range,
+    pipeline_shard,
+    reduce_pipeline,
 )
 from .mps import (
     EXACT,

@@ -14,7 +14,8 @@ LIB_NAME = "libtepai_b200.so"
 LIB_PATH = os.environ.get("TB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 EXPORTED = (
-    "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_debug_profile", "tb_run_stream",
+    "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_take_status", "tb_debug_profile",
+    "tb_run_stream",
     "tb_expectation", "tb_svd", "tb_svd_trunc", "tb_run_ensemble", "tb_run_ensemble_device", "tb_step", "tb_step_device",
 )
 
@@ -40,7 +41,7 @@ class EnsembleOut(ctypes.Structure):
     _fields_ = [
         ("values", ctypes.c_void_p), ("discarded", ctypes.c_void_p), ("ledger", ctypes.c_void_p),
         ("sum_v", ctypes.c_void_p), ("sum_v2", ctypes.c_void_p), ("flops", ctypes.c_void_p),
-        ("kernel_ms", ctypes.c_void_p),
+        ("kernel_ms", ctypes.c_void_p), ("excluded", ctypes.c_void_p),
     ]
 
 
@@ -72,6 +73,7 @@ def load() -> ctypes.CDLL:
         lib.tb_last_error.restype = ctypes.c_char_p
         lib.tb_num_sms.argtypes = [vp]
         lib.tb_debug_profile.argtypes = [vp, vp]
+        lib.tb_take_status.argtypes = [vp, vp]
         lib.tb_run_stream.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp, vp, vp, i64, i64, dbl, vp, vp]
         lib.tb_expectation.argtypes = [vp, vp, i64, i64, vp, vp, vp]
         lib.tb_svd.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp]
@@ -99,6 +101,36 @@ def context(device: int = 0) -> ctypes.c_void_p:
         return ctx
 
 
+class PrivateContext:
+    """An engine context owned by one object (a ``SlotPipeline``): its slot
+    pool is never touched by any other engine call.  Destroyed with its owner."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        self.ctx = ctypes.c_void_p()
+        rc = lib.tb_create(int(device), ctypes.byref(self.ctx))
+        if rc != 0 or not self.ctx.value:
+            raise RuntimeError(f"tb_create(device={device}) failed ({rc}): no usable CUDA device for the B200 engine")
+
+    def close(self) -> None:
+        if self.ctx is not None and self.ctx.value:
+            load().tb_destroy(self.ctx)
+        self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def take_status(ctx) -> int:
+    """Read and clear the sticky device status word (see tb_take_status)."""
+    st = ctypes.c_int32(0)
+    check(load().tb_take_status(ctx, ctypes.byref(st)), ctx)
+    return int(st.value)
+
+
 def check(rc: int, ctx) -> None:
     if rc == 0:
         return
@@ -112,9 +144,10 @@ def ptr(a: np.ndarray) -> int:
     return a.ctypes.data if a is not None else None
 
 
-def debug_profile(device: int = 0) -> np.ndarray:
-    """Phase cycle counters of the last ensemble launch (see tb_debug_profile)."""
+def debug_profile(device: int = 0, ctx=None) -> np.ndarray:
+    """Phase cycle counters of the last ensemble launch (see tb_debug_profile;
+    collected only when TB_PROFILE=1 was set before the context was created)."""
     out = np.zeros(64, np.uint64)
-    ctx = context(device)
+    ctx = ctx if ctx is not None else context(device)
     check(load().tb_debug_profile(ctx, out.ctypes.data), ctx)
     return out

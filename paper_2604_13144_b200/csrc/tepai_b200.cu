@@ -77,6 +77,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 struct Job {
   int n, cap, chi_cut, pi_local;
   int precond;  // QR-preconditioned Jacobi for problems >= 32 x 32
+  int max_sweeps;  // Jacobi sweep cap (TB_MAX_SWEEPS, tests of the non-convergence path only)
   int tail_skip;  // skip pairs of discarded-tail columns (see mark_tail)
   int qrcp_tmem;  // QR preconditioner with the matrix in tensor memory (qrcp_tmem)
   double floor;
@@ -104,7 +105,11 @@ struct Job {
   double* flops;       // [gridDim.x]
   unsigned long long* prof;  // [16] clock64 phase counters (diagnostics)
   int* next_sample;
-  int* status;         // bit 0: Jacobi non-convergence, bit 1: bad dims
+  int* status;         // bit 0: Jacobi non-convergence, bit 2: continued a slot of another generation
+  int* excluded;       // [n_samples] first checkpoint left out of the sums (non-convergence), -1: none; or NULL
+  unsigned char* slot_bad;  // [slots] the slot's current circuit hit a non-converged SVD (slot mode)
+  unsigned* slot_gen;       // [slots] workspace generation the slot's state was built in
+  unsigned gen;             // current workspace generation
   // run_stream mode i/o
   int* slot_dims;        // [slots][MAXN+1] persistent slot state (slot mode)
   int* slot_center;      // [slots]
@@ -140,6 +145,8 @@ struct Smem {
   double offmax;
   int k;
   int flag;
+  int bad;                   // this sample hit a non-converged SVD: its later checkpoints stay out of the sums
+  int maxsweep;              // Jacobi sweep cap (MAXSWEEP; lowered only by the failure-path tests)
   int sweeps;
   int rotcount;
   uint32_t tmem;             // TMEM base address (512 columns, allocated per CTA)
@@ -1102,7 +1109,7 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   if (threadIdx.x == 0) sm.ntail = 0;
   int sweep = 0;
   bool conv = false;
-  for (; sweep < MAXSWEEP; ++sweep) {
+  for (; sweep < sm.maxsweep; ++sweep) {
     const long long ts0 = prof_clock();
     J.refresh_norms(sm, tol, sweep == 0);
     if (sweep == 1) mark_tail(sm, JB * J.nblk, live);
@@ -1433,7 +1440,7 @@ __device__ int jacobi_wide(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   __syncthreads();
   int sweep = 0;
   bool conv = false;
-  for (; sweep < MAXSWEEP; ++sweep) {
+  for (; sweep < sm.maxsweep; ++sweep) {
     J.fold_and_norms(sm, tol, sweep == 0);
     if (sweep == 1) mark_tail(sm, Nw, live);
     J.sweep(sm);
@@ -1475,7 +1482,10 @@ __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* 
     neff = (sw > MAXSWEEP) ? -Nw : Nw;
   }
   if (neff < 0) {
-    if (threadIdx.x == 0) atomicOr(status, 1);
+    if (threadIdx.x == 0) {
+      atomicOr(status, 1);
+      sm.bad = 1;
+    }
     neff = -neff;
   }
   return neff;
@@ -2612,9 +2622,15 @@ __device__ void record_checkpoint(const Ctx& cx, Smem& sm, int sample, int ck) {
   measure_z(cx, sm);
   prof_add(jb, 6, prof_clock() - t0);
   const double sign = jb.ckpt_sign ? (double)jb.ckpt_sign[(size_t)sample * jb.n_ckpt + ck] : 1.0;
+  // a sample whose circuit hit a non-converged SVD keeps its raw values but
+  // contributes nothing from that checkpoint on; the caller learns which
+  // checkpoint through `excluded` and drops it from that row's count
+  const bool bad = sm.bad != 0;
+  if (bad && threadIdx.x == 0 && jb.excluded) atomicMin(&jb.excluded[sample], ck);
   for (int o = threadIdx.x; o < jb.n_obs; o += NT) {
     const double z = sm.zval[jb.obs_sites[o]];
     if (jb.values) jb.values[((size_t)sample * jb.n_ckpt + ck) * jb.n_obs + o] = z;
+    if (bad) continue;
     const double v = sign * z;
     const long long qv = llrint(v * FIX);
     const long long qv2 = llrint(z * z * FIX);
@@ -2645,6 +2661,8 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
     sm.flops = 0.0;
     sm.prof = job.prof;
     sm.tmem_on = job.qrcp_tmem;
+    sm.bad = 0;
+    sm.maxsweep = job.max_sweeps;
   }
   if (job.qrcp_tmem) tmem_alloc(sm);
   for (int iter = 0;; ++iter) {
@@ -2664,6 +2682,15 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
     int* sdims = job.slot_dims + (size_t)sample * (MAXN + 1);
     // --- initial state: product state, or the slot's persistent state
     const bool fresh = !job.slot_mode || (job.reset && job.reset[sample]);
+    if (job.slot_mode && !fresh && job.slot_gen[sample] != job.gen) {
+      // the slot's state was built in another workspace generation (the pool
+      // was reallocated or reshaped, or another engine call reused it): refuse
+      // to continue it rather than read stale memory
+      if (threadIdx.x == 0) atomicOr(job.status, 4);
+      __syncthreads();
+      continue;
+    }
+    if (threadIdx.x == 0) sm.bad = (job.slot_mode && !fresh) ? (int)job.slot_bad[sample] : 0;
     if (fresh && job.init_mps) {
       // hybrid fan-out: every sample starts from the broadcast snapshot
       for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = job.init_dims[e];
@@ -2758,6 +2785,8 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
       if (job.slot_mode) {
         job.slot_center[sample] = sm.center;
         for (int q = 0; q < 4; ++q) job.slot_counters[(size_t)sample * 4 + q] = sm.counters[q];
+        job.slot_bad[sample] = (unsigned char)sm.bad;
+        job.slot_gen[sample] = job.gen;
       }
     }
     if (job.slot_mode)
@@ -2832,6 +2861,7 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
     sm.prof = prof;
     sm.kcut = (kcut > 0 && kcut < K) ? kcut : MAXDIM;
     sm.tmem_on = (precond >> 1) & 1;
+    sm.maxsweep = MAXSWEEP;
   }
   if (precond & 2) tmem_alloc(sm);
   double2* W = Wg + mat_stride * b;
@@ -2906,10 +2936,17 @@ struct tb_ctx {
   int* slot_dims = nullptr;
   int* slot_center = nullptr;
   double* slot_counters = nullptr;
+  unsigned char* slot_bad = nullptr;
+  unsigned* slot_gen = nullptr;
+  // Workspace generation: bumped whenever the slot pool is reallocated,
+  // reshaped, or overwritten by a non-slot call (run_stream, run_ensemble,
+  // svd).  A slot continued (reset = 0) with a stale generation is refused.
+  unsigned gen = 1;
   size_t mps_cap_bytes = 0, mat_cap_bytes = 0;  // per slot
   int slots = 0;
   size_t mps_stride = 0, mat_stride = 0;
   int state_n = -1, state_cap = -1;  // shape the slot states were built for
+  bool profile = false;              // TB_PROFILE=1: clock64 phase counters (diagnostics only)
   // small device scratch
   int* dscratch = nullptr;  // [0] next_sample, [1] status
   double* dflops = nullptr;
@@ -2938,9 +2975,14 @@ void free_workspace(tb_ctx* c) {
   cudaFree(c->slot_dims);
   cudaFree(c->slot_center);
   cudaFree(c->slot_counters);
+  cudaFree(c->slot_bad);
+  cudaFree(c->slot_gen);
   c->mps = c->W = c->W0 = c->X = nullptr;
   c->slot_dims = c->slot_center = nullptr;
   c->slot_counters = nullptr;
+  c->slot_bad = nullptr;
+  c->slot_gen = nullptr;
+  ++c->gen;
   c->slots = 0;
   c->mps_cap_bytes = c->mat_cap_bytes = 0;
   c->state_n = c->state_cap = -1;
@@ -2955,7 +2997,10 @@ int ensure_workspace(tb_ctx* c, int slots, int n, int cap) {
   c->mps_stride = mps_bytes / sizeof(double2);
   c->mat_stride = mat_bytes / sizeof(double2);
   if (slots <= c->slots && mps_bytes <= c->mps_cap_bytes && mat_bytes <= c->mat_cap_bytes) {
-    if (n != c->state_n || cap != c->state_cap) c->state_n = c->state_cap = -1;
+    if (n != c->state_n || cap != c->state_cap) {
+      c->state_n = c->state_cap = -1;
+      ++c->gen;
+    }
     return TB_OK;
   }
   const int s = slots > c->slots ? slots : c->slots;
@@ -2966,7 +3011,10 @@ int ensure_workspace(tb_ctx* c, int slots, int n, int cap) {
       cudaMalloc(&c->W0, tb * s) != cudaSuccess || cudaMalloc(&c->X, tb * s) != cudaSuccess ||
       cudaMalloc(&c->slot_dims, (size_t)s * (tb::MAXN + 1) * sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->slot_center, (size_t)s * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&c->slot_counters, (size_t)s * 4 * sizeof(double)) != cudaSuccess) {
+      cudaMalloc(&c->slot_counters, (size_t)s * 4 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->slot_bad, (size_t)s) != cudaSuccess || cudaMalloc(&c->slot_gen, (size_t)s * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(c->slot_gen, 0, (size_t)s * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(c->slot_bad, 0, (size_t)s) != cudaSuccess) {
     cudaGetLastError();
     free_workspace(c);
     return fail(c, TB_ENOMEM, "workspace allocation failed");
@@ -3014,6 +3062,9 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
     job.tail_skip = ts ? atoi(ts) : 1;
     const char* tm = getenv("TB_QRCP_TMEM");
     job.qrcp_tmem = tm ? atoi(tm) : 1;
+    const char* ms = getenv("TB_MAX_SWEEPS");
+    job.max_sweeps = ms ? atoi(ms) : tb::MAXSWEEP;
+    if (job.max_sweeps < 1 || job.max_sweeps > tb::MAXSWEEP) job.max_sweeps = tb::MAXSWEEP;
   }
   job.floor = d->svalue_floor;
   job.n_samples = d->n_samples;
@@ -3035,9 +3086,13 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
   job.sum_v = (unsigned long long*)o->sum_v;
   job.sum_v2 = (unsigned long long*)o->sum_v2;
   job.flops = c->dflops;
-  job.prof = c->dprof;
+  job.prof = c->profile ? c->dprof : nullptr;  // phase atomics only in diagnostic runs
   job.next_sample = c->dscratch;
   job.status = c->dscratch + 1;
+  job.excluded = o->excluded;
+  job.slot_bad = c->slot_bad;
+  job.slot_gen = c->slot_gen;
+  job.gen = c->gen;
   job.slot_dims = c->slot_dims;
   job.slot_center = c->slot_center;
   job.slot_counters = c->slot_counters;
@@ -3054,7 +3109,7 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
 int launch(tb_ctx* c, tb::Job& job, int grid, cudaStream_t st, double* o_flops, float* kernel_ms) {
   const size_t smem = tb::kDynSmem;
   TB_CUDA(c, cudaFuncSetAttribute(tb::ensemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  TB_CUDA(c, cudaMemsetAsync(c->dscratch, 0, 2 * sizeof(int), st));
+  TB_CUDA(c, cudaMemsetAsync(c->dscratch, 0, sizeof(int), st));  // queue head; the status word stays sticky
   TB_CUDA(c, cudaMemsetAsync(c->dflops, 0, grid * sizeof(double), st));
   TB_CUDA(c, cudaMemsetAsync(c->dprof, 0, 64 * sizeof(unsigned long long), st));
   if (kernel_ms) TB_CUDA(c, cudaEventRecord(c->e0, st));
@@ -3072,11 +3127,32 @@ int launch(tb_ctx* c, tb::Job& job, int grid, cudaStream_t st, double* o_flops, 
   return TB_OK;
 }
 
-int read_status(tb_ctx* c) {
-  int st[2] = {0, 0};
-  TB_CUDA(c, cudaMemcpy(st, c->dscratch, sizeof(st), cudaMemcpyDeviceToHost));
-  if (st[1] & 1) return fail(c, TB_ENOCONV, "Jacobi SVD did not converge");
+// Read and clear the sticky device status word (bit 0: a Jacobi SVD did not
+// converge; bit 2: a slot of another workspace generation was continued).
+int take_status(tb_ctx* c, int* out) {
+  int st = 0;
+  TB_CUDA(c, cudaMemcpy(&st, c->dscratch + 1, sizeof(int), cudaMemcpyDeviceToHost));
+  TB_CUDA(c, cudaMemset(c->dscratch + 1, 0, sizeof(int)));
+  *out = st;
   return TB_OK;
+}
+
+// status -> return code; `nonconv_ok`: the caller receives per-sample
+// exclusion flags, so a non-converged sample is reported there instead
+int status_rc(tb_ctx* c, int st, bool nonconv_ok) {
+  if (st & 4)
+    return fail(c, TB_EINVAL,
+                "a slot was continued (reset = 0) after its workspace was reallocated, reshaped or reused by "
+                "another engine call; reset every slot");
+  if ((st & 1) && !nonconv_ok)
+    return fail(c, TB_ENOCONV, "Jacobi SVD did not converge (pass tb_ensemble_out.excluded to keep the launch)");
+  return TB_OK;
+}
+
+int read_status(tb_ctx* c, bool nonconv_ok = false) {
+  int st = 0;
+  const int rc = take_status(c, &st);
+  return rc ? rc : status_rc(c, st, nonconv_ok);
 }
 
 // device copies of a host descriptor/outputs; frees on destruction
@@ -3085,12 +3161,20 @@ struct Staged {
   ~Staged() {
     for (void* p : allocs) cudaFree(p);
   }
+  // device copy of h[0:count] (or uninitialised when !copy); NULL on any
+  // allocation or copy failure (the caller reports TB_ENOMEM / TB_ECUDA)
   template <class T>
   T* up(const T* h, size_t count, bool copy = true) {
     void* p = nullptr;
-    if (cudaMalloc(&p, count ? count * sizeof(T) : 8) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&p, count ? count * sizeof(T) : 8) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
     allocs.push_back(p);
-    if (copy && h && count) cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice);
+    if (copy && h && count && cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
     return (T*)p;
   }
 };
@@ -3126,9 +3210,12 @@ int stage_outputs(tb_ctx* c, Staged& sg, const tb_ensemble_desc* d, const tb_ens
   (void)rows;
   od->flops = sg.up<double>(nullptr, 1, false);
   od->kernel_ms = o->kernel_ms;
-  if ((o->values && !od->values) || (o->discarded && !od->discarded) || (o->ledger && !od->ledger) || !od->flops)
+  od->excluded = o->excluded ? sg.up<int32_t>(nullptr, (size_t)S, false) : nullptr;
+  if ((o->values && !od->values) || (o->discarded && !od->discarded) || (o->ledger && !od->ledger) || !od->flops ||
+      (o->excluded && !od->excluded))
     return fail(c, TB_ENOMEM, "device allocation failed");
   TB_CUDA(c, cudaMemset(od->flops, 0, sizeof(double)));
+  if (od->excluded) TB_CUDA(c, cudaMemset(od->excluded, 0xFF, (size_t)S * sizeof(int32_t)));  // -1: none
   return TB_OK;
 }
 
@@ -3140,6 +3227,7 @@ int fetch_outputs(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o, cons
   if (o->ledger) TB_CUDA(c, cudaMemcpy(o->ledger, od->ledger, (size_t)S * 4 * sizeof(double), cudaMemcpyDeviceToHost));
   TB_CUDA(c, cudaMemcpy(o->sum_v, od->sum_v, sum_rows * O * sizeof(int64_t), cudaMemcpyDeviceToHost));
   TB_CUDA(c, cudaMemcpy(o->sum_v2, od->sum_v2, sum_rows * O * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (o->excluded) TB_CUDA(c, cudaMemcpy(o->excluded, od->excluded, (size_t)S * sizeof(int32_t), cudaMemcpyDeviceToHost));
   double f = 0;
   TB_CUDA(c, cudaMemcpy(&f, od->flops, sizeof(double), cudaMemcpyDeviceToHost));
   o->flops[0] += f;
@@ -3163,6 +3251,10 @@ int tb_create(int device, tb_ctx** out) {
     return TB_ECUDA;
   }
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  {
+    const char* pf = getenv("TB_PROFILE");
+    c->profile = pf && atoi(pf) != 0;
+  }
   if (cudaMalloc(&c->dscratch, 256 * sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->dflops, 4096 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->dprof, 64 * sizeof(unsigned long long)) != cudaSuccess ||
@@ -3172,6 +3264,7 @@ int tb_create(int device, tb_ctx** out) {
     return TB_ECUDA;
   }
   cudaMemset(c->dprof, 0, 64 * sizeof(unsigned long long));
+  cudaMemset(c->dscratch, 0, 256 * sizeof(int));
   *out = c;
   return TB_OK;
 }
@@ -3190,6 +3283,14 @@ void tb_destroy(tb_ctx* c) {
 const char* tb_last_error(const tb_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int tb_num_sms(const tb_ctx* c) { return c ? c->sms : 0; }
+
+int tb_take_status(tb_ctx* c, int32_t* status) {
+  if (!c || !status) return TB_EINVAL;
+  int st = 0;
+  const int rc = take_status(c, &st);
+  *status = st;
+  return rc;
+}
 
 int tb_debug_profile(tb_ctx* c, uint64_t* out64) {
   if (!c || !out64) return TB_EINVAL;
@@ -3244,6 +3345,8 @@ int tb_run_stream(tb_ctx* c, double* buf, int64_t n, int64_t cap, int64_t* dims,
   TB_CUDA(c, cudaMemcpy(c->slot_center, &icenter, sizeof(int), cudaMemcpyHostToDevice));
   TB_CUDA(c, cudaMemcpy(c->slot_counters, counters, 4 * sizeof(double), cudaMemcpyHostToDevice));
   TB_CUDA(c, cudaMemcpy(c->mps, buf, site_bytes, cudaMemcpyHostToDevice));
+  TB_CUDA(c, cudaMemcpy(c->slot_gen, &c->gen, sizeof(unsigned), cudaMemcpyHostToDevice));
+  TB_CUDA(c, cudaMemset(c->slot_bad, 0, 1));
   tb_ensemble_desc d;
   memset(&d, 0, sizeof(d));
   d.n = (int)n;
@@ -3269,6 +3372,7 @@ int tb_run_stream(tb_ctx* c, double* buf, int64_t n, int64_t cap, int64_t* dims,
   for (int64_t s = 0; s <= n; ++s) dims[s] = idims[(size_t)s];
   *new_center = icenter;
   c->state_n = c->state_cap = -1;  // slot 0 now holds a caller's state, not a pipeline slot
+  ++c->gen;
   return read_status(c);
 }
 
@@ -3315,6 +3419,7 @@ int tb_svd_trunc(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n
   int rc = ensure_workspace(c, (int)batch, 1, cap < 1 ? 1 : cap);
   if (rc) return rc;
   c->state_n = c->state_cap = -1;
+  ++c->gen;
   Staged sg;
   double2* da = sg.up((const double2*)a, (size_t)(batch * m * n));
   double* ds = sg.up<double>(nullptr, (size_t)(batch * k), false);
@@ -3323,6 +3428,7 @@ int tb_svd_trunc(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n
   if (!da || !ds || (u && !du) || (vh && !dvh)) return fail(c, TB_ENOMEM, "device allocation failed");
   TB_CUDA(c, cudaMemset(c->dscratch, 0, 2 * sizeof(int)));
   TB_CUDA(c, cudaMemset(c->dprof, 0, 64 * sizeof(unsigned long long)));
+  // tb_svd has no per-sample flags: its status is this call's alone
   const size_t smem = tb::kDynSmem;
   TB_CUDA(c, cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const char* pe = getenv("TB_PRECOND");
@@ -3347,6 +3453,7 @@ int tb_run_ensemble_device(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out
   rc = ensure_workspace(c, grid, d->n, d->cap);
   if (rc) return rc;
   c->state_n = c->state_cap = -1;  // whole-sample runs reuse the slot memory
+  ++c->gen;
   tb::Job job = make_job(c, d, o);
   job.slot_mode = 0;
   return launch(c, job, grid, (cudaStream_t)stream, o->flops, o->kernel_ms);
@@ -3368,8 +3475,9 @@ int tb_run_ensemble(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o) {
   rc = tb_run_ensemble_device(c, &dd, &od, nullptr);
   if (rc) return rc;
   TB_CUDA(c, cudaDeviceSynchronize());
-  if ((rc = fetch_outputs(c, d, o, &od, rows))) return rc;
-  return read_status(c);
+  // the caller's arrays (accumulated sums included) change only on success
+  if ((rc = read_status(c, o->excluded != nullptr))) return rc;
+  return fetch_outputs(c, d, o, &od, rows);
 }
 
 int tb_step_device(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, void* stream) {
@@ -3417,8 +3525,8 @@ int tb_step(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, int64_t sum_r
   rc = tb_step_device(c, &sdd, &od, nullptr);
   if (rc) return rc;
   TB_CUDA(c, cudaDeviceSynchronize());
-  if ((rc = fetch_outputs(c, d, o, &od, (size_t)sum_rows))) return rc;
-  return read_status(c);
+  if ((rc = read_status(c, o->excluded != nullptr))) return rc;
+  return fetch_outputs(c, d, o, &od, (size_t)sum_rows);
 }
 
 }  // extern "C"

@@ -98,21 +98,22 @@ def aggregate(records) -> EnsembleResult:
     return res
 
 
-def aggregate_fixed(sum_v: np.ndarray, sum_v2: np.ndarray, n_samples: int, g_norm: np.ndarray):
+def aggregate_fixed(sum_v: np.ndarray, sum_v2: np.ndarray, n_samples, g_norm: np.ndarray):
     """Statistics from the device's fixed-point sums: arrays [C, O] of int64,
-    g_norm [C].  Returns dict of float arrays (mean, std_error, var_o, var_v)."""
-    if n_samples < 1:
+    g_norm [C]; ``n_samples`` is one count or one per checkpoint row [C] (rows
+    can differ when the engine left a non-converged sample out).  Returns dict
+    of float arrays (mean, std_error, var_o, var_v)."""
+    ns = np.asarray(n_samples, dtype=np.int64)
+    if ns.size == 0 or int(ns.min()) < 1:
         raise ValueError("aggregate needs at least one sample")
     sv = np.asarray(sum_v, dtype=np.int64).astype(np.float64) / FIX
     sv2 = np.asarray(sum_v2, dtype=np.int64).astype(np.float64) / FIX
     g = np.asarray(g_norm, dtype=np.float64).reshape(-1, 1)
-    mean_v = sv / n_samples
-    if n_samples > 1:
-        var_v = np.maximum((sv2 - n_samples * mean_v * mean_v) / (n_samples - 1), 0.0)
-    else:
-        var_v = np.zeros_like(sv)
+    n = ns.astype(np.float64).reshape(-1, 1) if ns.ndim else float(ns)
+    mean_v = sv / n
+    var_v = np.where(n > 1, np.maximum((sv2 - n * mean_v * mean_v) / np.maximum(n - 1, 1), 0.0), 0.0)
     var_o = g * g * var_v
-    return {"estimate": g * mean_v, "std_error": np.sqrt(var_o / n_samples), "var_o": var_o, "var_v": var_v,
+    return {"estimate": g * mean_v, "std_error": np.sqrt(var_o / n), "var_o": var_o, "var_v": var_v,
             "mean_v": mean_v}
 
 

@@ -1,0 +1,141 @@
+"""Truncated-regime golden fixtures for the statistical parity harness
+(SURVEY.md §4 test 3, §8(c) criteria (i)-(iii); VERDICT r01 "next" item 1).
+
+Runs the UNMODIFIED reference ``tepai`` package (``/root/reference/pkg/src``,
+un-jitted because its numba kernel does not compile under numba 0.65, SURVEY
+§0 fact 4) on the C2 and C3 configurations for every sample id in a range, at
+all 20 prefix checkpoints (SURVEY §8(a) checkpoint semantics: one
+``run_circuit`` per checkpoint interval, then the reference's own
+``expectation`` for every Z_j).
+
+Each sample runs twice:
+  * ``gesdd`` -- the reference exactly as shipped (``np.linalg.svd`` at
+    ``_kernel.py:117`` is LAPACK zgesdd);
+  * ``gesvd`` -- the same gate list with that one call swapped for LAPACK
+    zgesvd (``scipy.linalg.svd(..., lapack_driver="gesvd")``), the
+    ref-vs-ref spread of SURVEY §0 fact 6 / Appendix A.5.  The swap is a
+    module-attribute shim in the worker process; no reference file changes.
+
+Writes ``tests/golden/ref_c2_stat.npz`` (256 samples) and
+``tests/golden/ref_c3_stat.npz`` (64 samples).  Per-sample partial results
+are cached under /tmp/golden_trunc so an interrupted run resumes.
+
+Usage:  python tests/golden/make_golden_trunc.py [--procs 7]
+Cost:   ~46k CPU-s (C3 ~273 s per sample and driver un-jitted).
+"""
+
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import math
+import os
+import sys
+import types
+
+os.environ.setdefault("NUMBA_DISABLE_JIT", "1")
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+sys.dont_write_bytecode = True
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+import numpy as np  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CACHE = "/tmp/golden_trunc"
+DELTA = math.pi / 2**7
+CONFIGS = {
+    # name: (n, ham_seed, circ_seed, n_steps, T, chi, n_samples)
+    "c2": (16, 2, 3, 200, 2.0, 32, 256),
+    "c3": (32, 4, 5, 200, 2.0, 64, 64),
+}
+N_CKPT, EVERY = 20, 10
+
+
+def _install_gesvd():
+    """Swap the reference kernel's ``np.linalg.svd`` for zgesvd (this process only)."""
+    import scipy.linalg
+    from tepai import _kernel
+
+    def svd(a, full_matrices=True):
+        return scipy.linalg.svd(a, full_matrices=full_matrices, lapack_driver="gesvd", check_finite=False)
+
+    shim = types.SimpleNamespace(**{k: getattr(np, k) for k in dir(np) if not k.startswith("__")})
+    shim.linalg = types.SimpleNamespace(svd=svd, qr=np.linalg.qr)
+    _kernel.np = shim
+
+
+def run_member(args):
+    name, sid, driver = args
+    path = os.path.join(CACHE, f"{name}_{driver}_{sid}.npz")
+    if os.path.exists(path):
+        return path
+    import tepai
+    from tepai import rng as trng
+    if driver == "gesvd":
+        _install_gesvd()
+    n, hs, cs, steps, T, chi, _ = CONFIGS[name]
+    ham = tepai.build_spin_ring(n, 1.0, hs)
+    circ = tepai.sample_circuit(ham, tepai.PaiConfig(DELTA, steps, T), trng.circuit_stream(cs, sid), sample_id=sid)
+    state = tepai.init_product_state("01" * (n // 2))
+    policy = tepai.TruncationPolicy(chi_cut=chi, svalue_floor=1e-12)
+    ledger = tepai.CostLedger()
+    zs = [tepai.PauliString.single(n, q, "Z") for q in range(n)]
+    vals = np.zeros((N_CKPT, n))
+    disc = np.zeros(N_CKPT)
+    sign = np.zeros(N_CKPT, np.int64)
+    lo = 0
+    for ci in range(N_CKPT):
+        j = (ci + 1) * EVERY
+        hi = int(np.searchsorted(circ.step_index, j, side="left"))
+        seg = dataclasses.replace(circ, term_index=circ.term_index[lo:hi], step_index=circ.step_index[lo:hi],
+                                  kinds=circ.kinds[lo:hi], signs=circ.signs[lo:hi])
+        tepai.run_circuit(state, seg, policy, ledger)
+        lo = hi
+        vals[ci] = [tepai.expectation(state, z) for z in zs]
+        disc[ci] = tepai.discarded_weight(state)
+        sign[ci] = 1 - 2 * (int(np.count_nonzero(circ.kinds[:hi] == 2)) & 1)
+    os.makedirs(CACHE, exist_ok=True)
+    tmp = path + ".part.npz"
+    np.savez(tmp, vals=vals, disc=disc, sign=sign,
+             ledger=np.array([ledger.gate_count, ledger.sum_chi_cubed, ledger.chi_max], np.float64))
+    os.replace(tmp, path)
+    return path
+
+
+def assemble(name):
+    import tepai
+    n, hs, cs, steps, T, chi, count = CONFIGS[name]
+    ham = tepai.build_spin_ring(n, 1.0, hs)
+    weights = np.array([tepai.sampling.circuit_weight_norm(
+        ham, tepai.PaiConfig(DELTA, (c + 1) * EVERY, (c + 1) * EVERY * T / steps)) for c in range(N_CKPT)])
+    out = dict(sample_ids=np.arange(count), weights=weights, checkpoints=np.arange(1, N_CKPT + 1) * EVERY)
+    for driver in ("gesdd", "gesvd"):
+        rows = [np.load(os.path.join(CACHE, f"{name}_{driver}_{i}.npz")) for i in range(count)]
+        out[f"vals_{driver}"] = np.stack([r["vals"] for r in rows])
+        out[f"disc_{driver}"] = np.stack([r["disc"] for r in rows])
+        out[f"ledger_{driver}"] = np.stack([r["ledger"] for r in rows])
+        if driver == "gesdd":
+            out["sign"] = np.stack([r["sign"] for r in rows])
+    np.savez_compressed(os.path.join(HERE, f"ref_{name}_stat.npz"), **out)
+
+
+def main():
+    from multiprocessing import Pool
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--procs", type=int, default=max(1, (os.cpu_count() or 2) - 1))
+    ap.add_argument("--only", choices=sorted(CONFIGS), default=None)
+    a = ap.parse_args()
+    names = [a.only] if a.only else ["c3", "c2"]
+    jobs = [(nm, i, d) for nm in names for i in range(CONFIGS[nm][6]) for d in ("gesdd", "gesvd")]
+    with Pool(a.procs) as pool:
+        for k, p in enumerate(pool.imap_unordered(run_member, jobs, chunksize=1)):
+            print(f"[{k + 1}/{len(jobs)}] {os.path.basename(p)}", flush=True)
+    for nm in names:
+        assemble(nm)
+    print("written:", [f"ref_{nm}_stat.npz" for nm in names])
+
+
+if __name__ == "__main__":
+    main()

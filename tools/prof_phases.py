@@ -1,4 +1,5 @@
 """Cycle breakdown of the batched 128x128 SVD kernel (diagnostic counters)."""
+import os; os.environ.setdefault("TB_PROFILE", "1")  # phase counters are diagnostics-only
 import sys, numpy as np
 sys.path.insert(0, ".")
 from paper_2604_13144_b200 import _lib

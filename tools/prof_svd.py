@@ -1,5 +1,6 @@
 """Batched 128x128 complex SVD through tb_svd (one CTA per matrix) — the
 Jacobi kernel in isolation, for timing and ncu.  usage: prof_svd.py [batch] [reps] [m] [n]"""
+import os; os.environ.setdefault("TB_PROFILE", "1")  # phase counters are diagnostics-only
 import sys, time
 import numpy as np
 sys.path.insert(0, ".")

@@ -1,4 +1,5 @@
 """Timing + phase counters of the wide (256-row) SVD path (diagnostic)."""
+import os; os.environ.setdefault("TB_PROFILE", "1")  # phase counters are diagnostics-only
 import sys, time
 import numpy as np
 sys.path.insert(0, ".")

@@ -1,6 +1,7 @@
 """Load balance of the slot-mode step (bench definition): per launch, kernel
 time vs the mean per-CTA busy time (clock64 counter prof[7] / CTAs / clock).
 usage: python tools/slot_balance.py [steps] [slots]"""
+import os; os.environ.setdefault("TB_PROFILE", "1")  # phase counters are diagnostics-only
 import math, sys
 import numpy as np
 sys.path.insert(0, ".")
@@ -14,10 +15,10 @@ ham = tb.build_spin_ring(32, 1.0, 4)
 cfg = tb.PaiConfig(math.pi / 2**7, 200, 2.0)
 pipe = SlotPipeline(ham, cfg, 5, "01" * 16, tb.TruncationPolicy(64, 1e-12), np.arange(10, 201, 10), n_slots=slots)
 ctas = min(pipe.n_slots, 148)
-prev = _lib.debug_profile().astype(np.float64)
+prev = _lib.debug_profile(ctx=pipe.ctx).astype(np.float64)
 for i in range(steps):
     ms = pipe.step_host(pipe.plan())
-    pr = _lib.debug_profile().astype(np.float64)
+    pr = _lib.debug_profile(ctx=pipe.ctx).astype(np.float64)
     busy = pr[7] / ctas / 1.965e6  # the counters are reset per launch
     prev = pr
     print(f"step {i}: slots {pipe.n_slots} kernel {ms:.0f} ms, mean CTA busy {busy:.0f} ms, balance {busy / ms:.3f}")

@@ -1,5 +1,6 @@
 """Time the engine on a prefix of a config's circuits (exploration tool).
 usage: python tools/time_prefix.py N_SITES CHI HAM_SEED CIRC_SEED STEPS T N_SAMPLES MAX_STEP"""
+import os; os.environ.setdefault("TB_PROFILE", "1")  # phase counters are diagnostics-only
 import math, sys, time
 import numpy as np
 sys.path.insert(0, ".")

@@ -81,6 +81,14 @@ int tb_run_stream(tb_ctx* ctx, double* buf, int64_t n, int64_t cap, int64_t* dim
 int tb_expectation(tb_ctx* ctx, const double* buf, int64_t n, int64_t cap, const int64_t* dims,
                    const int32_t* pauli_codes, double* out);
 
+/* Batched <psi_s|P_o|psi_s> for S states and O Pauli strings (transfer
+ * contraction as mps.expectation, mps.py:170-182): the one-pass evaluation of
+ * a signed mixture's observables (evaluate_observables).
+ * bufs: complex128 [S][n][cap][2][cap]; dims: int64 [S][n+1];
+ * codes: int32 [O][n] (0=I, 1=X, 2=Y, 3=Z); out: float64 [S][O]. */
+int tb_expectation_batch(tb_ctx* ctx, const double* bufs, int64_t n_states, int64_t n, int64_t cap,
+                         const int64_t* dims, const int32_t* codes, int64_t n_obs, double* out);
+
 /* Batched thin SVD (unit-test surface of the Jacobi kernel).
  * a: complex128 [batch][m][n] row-major; s: [batch][k]; u: [batch][m][k];
  * vh: [batch][k][n] with k = min(m, n).  Any of u / vh may be NULL. */
@@ -139,6 +147,15 @@ typedef struct tb_ensemble_out {
    * leaves every caller array untouched.  Device calls: the caller fills it
    * with -1 before the launch. */
   int32_t* excluded;
+  /* Optional per-sample final states for the signed mixture:
+   * complex128 [n_samples][n][cap][2][cap] (zero-padded), bond dims
+   * [n_samples][n+1] and centres [n_samples]; NULL = not retained. */
+  double* states;
+  int32_t* state_dims;
+  int32_t* state_center;
+  /* [n_samples] device time (ms) of each sample (queue mode) or of its segment
+   * (slot mode): the measured C_circ of the cost report. */
+  double* sample_ms;
 } tb_ensemble_out;
 
 /* Host-buffer ensemble run: uploads the streams, runs the persistent kernel,

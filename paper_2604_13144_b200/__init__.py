@@ -5,7 +5,19 @@ Public names mirror ``pkg/src/tepai/__init__.py:11-52`` for the path in scope
 plus the batched ``run_ensemble`` / ``aggregate`` of SPEC.md.
 """
 
-from .estimator import EnsembleResult, SampleRecord, aggregate, aggregate_fixed, results_table
+from .estimator import (
+    EnsembleResult,
+    SampleRecord,
+    SignedMixture,
+    aggregate,
+    aggregate_fixed,
+    evaluate_observables,
+    mixture_from_run,
+    per_sample_expectations,
+    results_table,
+    variance_vs_bound_trace,
+)
+from .runner import CostReport, cost_report, cost_table, tts_tradeoff
 from .ensemble import (
     SlotPipeline,
     EnsembleRun,

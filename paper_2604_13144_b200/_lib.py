@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("TB_LIB") or os.path.join(os.path.dirname(os.path.absp
 EXPORTED = (
     "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_take_status", "tb_debug_profile",
     "tb_run_stream",
-    "tb_expectation", "tb_svd", "tb_svd_trunc", "tb_run_ensemble", "tb_run_ensemble_device", "tb_step", "tb_step_device",
+    "tb_expectation", "tb_expectation_batch", "tb_svd", "tb_svd_trunc", "tb_run_ensemble", "tb_run_ensemble_device", "tb_step", "tb_step_device",
 )
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -41,7 +41,8 @@ class EnsembleOut(ctypes.Structure):
     _fields_ = [
         ("values", ctypes.c_void_p), ("discarded", ctypes.c_void_p), ("ledger", ctypes.c_void_p),
         ("sum_v", ctypes.c_void_p), ("sum_v2", ctypes.c_void_p), ("flops", ctypes.c_void_p),
-        ("kernel_ms", ctypes.c_void_p), ("excluded", ctypes.c_void_p),
+        ("kernel_ms", ctypes.c_void_p), ("excluded", ctypes.c_void_p), ("states", ctypes.c_void_p),
+        ("state_dims", ctypes.c_void_p), ("state_center", ctypes.c_void_p), ("sample_ms", ctypes.c_void_p),
     ]
 
 
@@ -76,6 +77,7 @@ def load() -> ctypes.CDLL:
         lib.tb_take_status.argtypes = [vp, vp]
         lib.tb_run_stream.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp, vp, vp, i64, i64, dbl, vp, vp]
         lib.tb_expectation.argtypes = [vp, vp, i64, i64, vp, vp, vp]
+        lib.tb_expectation_batch.argtypes = [vp, vp, i64, i64, i64, vp, vp, i64, vp]
         lib.tb_svd.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp]
         if hasattr(lib, "tb_svd_trunc"):  # absent in pre-r01b builds (A/B timing of old libraries)
             lib.tb_svd_trunc.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp]

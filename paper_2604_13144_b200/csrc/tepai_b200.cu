@@ -110,6 +110,10 @@ struct Job {
   unsigned char* slot_bad;  // [slots] the slot's current circuit hit a non-converged SVD (slot mode)
   unsigned* slot_gen;       // [slots] workspace generation the slot's state was built in
   unsigned gen;             // current workspace generation
+  double2* states;          // [n_samples][n][cap][2][cap] final MPS per sample (signed mixture), or NULL
+  int* state_dims;          // [n_samples][n+1]
+  int* state_center;        // [n_samples]
+  double* sample_ms;        // [n_samples] device time of the sample (queue) / its segment (slot mode), or NULL
   // run_stream mode i/o
   int* slot_dims;        // [slots][MAXN+1] persistent slot state (slot mode)
   int* slot_center;      // [slots]
@@ -1633,8 +1637,9 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
       if (!valid) d = cz();
 #pragma unroll
       for (int q = 0; q < HR; ++q) {
-        y.v[q].x -= d.x * qv.v[q].x - d.y * qv.v[q].y;
-        y.v[q].y -= d.x * qv.v[q].y + d.y * qv.v[q].x;
+        // y -= d q as four fused multiply-adds (no DMUL/DADD pairs)
+        y.v[q].x = fma(-d.x, qv.v[q].x, fma(d.y, qv.v[q].y, y.v[q].x));
+        y.v[q].y = fma(-d.x, qv.v[q].y, fma(-d.y, qv.v[q].x, y.v[q].y));
       }
       double nr = valid ? sm.nrm[c] - abs2(d) : 0.0;
       const bool f = valid && nr < 1e-2 * sm.nref[c];
@@ -1855,8 +1860,9 @@ __device__ __noinline__ int qrcp_tmem(const double2* Y, int Nw, int Mw, double2*
       if (!valid) d = cz();
 #pragma unroll
       for (int q = 0; q < HR; ++q) {
-        y.v[q].x -= d.x * qv.v[q].x - d.y * qv.v[q].y;
-        y.v[q].y -= d.x * qv.v[q].y + d.y * qv.v[q].x;
+        // y -= d q as four fused multiply-adds (no DMUL/DADD pairs)
+        y.v[q].x = fma(-d.x, qv.v[q].x, fma(d.y, qv.v[q].y, y.v[q].x));
+        y.v[q].y = fma(-d.x, qv.v[q].y, fma(-d.y, qv.v[q].x, y.v[q].y));
       }
       double nr = valid ? sm.nrm[c] - abs2(d) : 0.0;
       const bool f = valid && nr < 1e-2 * sm.nref[c];
@@ -2044,8 +2050,9 @@ __device__ int qrcp_wide(double2* Y, int Nw, int Mw, double2* R, Smem& sm, doubl
 #pragma unroll
       for (int q = 0; q < HR; ++q) {
         const double2 qq = lds2(qaddr + l + 256u * q);
-        y.v[q].x -= d.x * qq.x - d.y * qq.y;
-        y.v[q].y -= d.x * qq.y + d.y * qq.x;
+        // y -= d q as four fused multiply-adds (no DMUL/DADD pairs)
+        y.v[q].x = fma(-d.x, qq.x, fma(d.y, qq.y, y.v[q].x));
+        y.v[q].y = fma(-d.x, qq.y, fma(-d.y, qq.x, y.v[q].y));
       }
       double nr = valid ? sm.nrm[c] - abs2(d) : 0.0;
       const bool f = valid && nr < 1e-2 * sm.nref[c];
@@ -2731,6 +2738,8 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
     }
     __syncthreads();
     const long long tstart = prof_clock();
+    unsigned long long ns0 = 0;
+    if (job.sample_ms && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns0));
     const int64_t g0 = job.gate_off[sample], g1 = job.gate_off[sample + 1];
     int ck = 0;
     for (int64_t gi = g0; gi < g1; ++gi) {
@@ -2779,6 +2788,26 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
       ++ck;
     }
     prof_add(job, 7, prof_clock() - tstart);
+    if (job.states) {
+      // retain the final MPS (zero-padded to cap x 2 x cap per site) for the
+      // signed-mixture post-processing
+      double2* dst = job.states + (size_t)sample * n * cap * 2 * cap;
+      for (int st = 0; st < n; ++st) {
+        const double2* src = cx.site(st);
+        const int cl = sm.dims[st], cr = sm.dims[st + 1];
+        for (int e = threadIdx.x; e < cap * 2 * cap; e += NT) {
+          const int row = e / cap, r = e - row * cap;
+          dst[(size_t)st * cap * 2 * cap + e] = ((row >> 1) < cl && r < cr) ? src[e] : cz();
+        }
+      }
+      for (int e = threadIdx.x; e <= n; e += NT) job.state_dims[(size_t)sample * (n + 1) + e] = sm.dims[e];
+      if (threadIdx.x == 0) job.state_center[sample] = sm.center;
+    }
+    if (job.sample_ms && threadIdx.x == 0) {
+      unsigned long long ns1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns1));
+      job.sample_ms[sample] = 1e-6 * (double)(ns1 - ns0);
+    }
     if (threadIdx.x == 0) {
       if (job.ledger)
         for (int q = 0; q < 4; ++q) job.ledger[(size_t)sample * 4 + q] = sm.counters[q];
@@ -2800,11 +2829,8 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
 // ----------------------------------------------------------------------------
 // transfer-contraction expectation of a general Pauli string (mps.py:170-182)
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 1) expectation_kernel(const double2* buf, int n, int cap, const int* dims,
-                                                            const int* codes, double2* E, double2* F, double* out) {
-  extern __shared__ double2 dyn_smem[];
-  __shared__ Smem sm;
-  for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = dims[e];
+__device__ double transfer_expect(const double2* buf, int n, int cap, const Smem& sm, const int* codes, double2* E,
+                                  double2* F, double2* tile) {
   if (threadIdx.x == 0) E[0] = make_double2(1.0, 0.0);
   __syncthreads();
   for (int k = 0; k < n; ++k) {
@@ -2818,7 +2844,7 @@ __global__ void __launch_bounds__(NT, 1) expectation_kernel(const double2* buf, 
           const int i = q / kr, r = q - i * kr;
           return T[(size_t)(l2 * 2 + i) * cap + r];
         },
-        [&](int l, int q, double2 v) { F[(size_t)l * K2 + q] = v; }, dyn_smem);
+        [&](int l, int q, double2 v) { F[(size_t)l * K2 + q] = v; }, tile);
     if (p != 0) {
       for (int e = threadIdx.x; e < kl * kr; e += NT) {
         const int l = e / kr, r = e - l * kr;
@@ -2841,9 +2867,45 @@ __global__ void __launch_bounds__(NT, 1) expectation_kernel(const double2* buf, 
           const int l = q >> 1, i = q & 1;
           return F[(size_t)l * K2 + i * kr + r2];
         },
-        [&](int a, int b, double2 v) { E[(size_t)a * kr + b] = v; }, dyn_smem);
+        [&](int a, int b, double2 v) { E[(size_t)a * kr + b] = v; }, tile);
   }
-  if (threadIdx.x == 0) out[0] = E[0].x;
+  const double v = E[0].x;
+  __syncthreads();
+  return v;
+}
+
+__global__ void __launch_bounds__(NT, 1) expectation_kernel(const double2* buf, int n, int cap, const int* dims,
+                                                            const int* codes, double2* E, double2* F, double* out) {
+  extern __shared__ double2 dyn_smem[];
+  __shared__ Smem sm;
+  for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = dims[e];
+  __syncthreads();
+  const double v = transfer_expect(buf, n, cap, sm, codes, E, F, dyn_smem);
+  if (threadIdx.x == 0) out[0] = v;
+}
+
+// Batched transfer-contraction expectations (the signed-mixture post-processing
+// of SPEC.md:413-417): states [S][n][cap][2][cap] with dims [S][n+1], Pauli
+// strings codes [O][n]; out [S][O].  Persistent CTAs stride over the states;
+// each CTA uses its own slice of the W / W0 scratch for the environments.
+__global__ void __launch_bounds__(NT, 1) expectation_batch_kernel(const double2* bufs, int S, int n, int cap,
+                                                                  const int* dims, const int* codes, int O,
+                                                                  double2* Ew, double2* Fw, size_t mat_stride,
+                                                                  double* out) {
+  extern __shared__ double2 dyn_smem[];
+  __shared__ Smem sm;
+  double2* E = Ew + mat_stride * blockIdx.x;
+  double2* F = Fw + mat_stride * blockIdx.x;
+  for (int st = blockIdx.x; st < S; st += gridDim.x) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < n + 1; e += NT) sm.dims[e] = dims[(size_t)st * (n + 1) + e];
+    __syncthreads();
+    const double2* buf = bufs + (size_t)st * n * cap * 2 * cap;
+    for (int o = 0; o < O; ++o) {
+      const double v = transfer_expect(buf, n, cap, sm, codes + (size_t)o * n, E, F, dyn_smem);
+      if (threadIdx.x == 0) out[(size_t)st * O + o] = v;
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -3090,6 +3152,10 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
   job.next_sample = c->dscratch;
   job.status = c->dscratch + 1;
   job.excluded = o->excluded;
+  job.states = (double2*)o->states;
+  job.state_dims = o->state_dims;
+  job.state_center = o->state_center;
+  job.sample_ms = o->sample_ms;
   job.slot_bad = c->slot_bad;
   job.slot_gen = c->slot_gen;
   job.gen = c->gen;
@@ -3211,8 +3277,14 @@ int stage_outputs(tb_ctx* c, Staged& sg, const tb_ensemble_desc* d, const tb_ens
   od->flops = sg.up<double>(nullptr, 1, false);
   od->kernel_ms = o->kernel_ms;
   od->excluded = o->excluded ? sg.up<int32_t>(nullptr, (size_t)S, false) : nullptr;
+  const size_t sbytes = (size_t)d->n * d->cap * 2 * d->cap;
+  od->states = o->states ? (double*)sg.up<double2>(nullptr, (size_t)S * sbytes, false) : nullptr;
+  od->state_dims = o->states ? sg.up<int32_t>(nullptr, (size_t)S * (d->n + 1), false) : nullptr;
+  od->state_center = o->states ? sg.up<int32_t>(nullptr, (size_t)S, false) : nullptr;
+  od->sample_ms = o->sample_ms ? sg.up<double>(nullptr, (size_t)S, false) : nullptr;
   if ((o->values && !od->values) || (o->discarded && !od->discarded) || (o->ledger && !od->ledger) || !od->flops ||
-      (o->excluded && !od->excluded))
+      (o->excluded && !od->excluded) || (o->states && (!od->states || !od->state_dims || !od->state_center)) ||
+      (o->sample_ms && !od->sample_ms))
     return fail(c, TB_ENOMEM, "device allocation failed");
   TB_CUDA(c, cudaMemset(od->flops, 0, sizeof(double)));
   if (od->excluded) TB_CUDA(c, cudaMemset(od->excluded, 0xFF, (size_t)S * sizeof(int32_t)));  // -1: none
@@ -3228,6 +3300,14 @@ int fetch_outputs(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o, cons
   TB_CUDA(c, cudaMemcpy(o->sum_v, od->sum_v, sum_rows * O * sizeof(int64_t), cudaMemcpyDeviceToHost));
   TB_CUDA(c, cudaMemcpy(o->sum_v2, od->sum_v2, sum_rows * O * sizeof(int64_t), cudaMemcpyDeviceToHost));
   if (o->excluded) TB_CUDA(c, cudaMemcpy(o->excluded, od->excluded, (size_t)S * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (o->states) {
+    const size_t sb = (size_t)d->n * d->cap * 2 * d->cap * sizeof(double2);
+    TB_CUDA(c, cudaMemcpy(o->states, od->states, (size_t)S * sb, cudaMemcpyDeviceToHost));
+    TB_CUDA(c, cudaMemcpy(o->state_dims, od->state_dims, (size_t)S * (d->n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    TB_CUDA(c, cudaMemcpy(o->state_center, od->state_center, (size_t)S * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
+  if (o->sample_ms)
+    TB_CUDA(c, cudaMemcpy(o->sample_ms, od->sample_ms, (size_t)S * sizeof(double), cudaMemcpyDeviceToHost));
   double f = 0;
   TB_CUDA(c, cudaMemcpy(&f, od->flops, sizeof(double), cudaMemcpyDeviceToHost));
   o->flops[0] += f;
@@ -3402,6 +3482,42 @@ int tb_expectation(tb_ctx* c, const double* buf, int64_t n, int64_t cap, const i
   tb::expectation_kernel<<<1, tb::NT, smem>>>(dbuf, (int)n, (int)cap, dd, dd + n + 1, c->W, c->W0, dout);
   TB_CUDA(c, cudaGetLastError());
   TB_CUDA(c, cudaMemcpy(out, dout, sizeof(double), cudaMemcpyDeviceToHost));
+  return TB_OK;
+}
+
+int tb_expectation_batch(tb_ctx* c, const double* bufs, int64_t n_states, int64_t n, int64_t cap, const int64_t* dims,
+                         const int32_t* codes, int64_t n_obs, double* out) {
+  if (!c) return TB_EINVAL;
+  int rc = validate_shape(c, n, cap, 1);
+  if (rc) return rc;
+  if (n_states < 0 || n_obs < 0 || (n_states > 0 && n_obs > 0 && (!bufs || !dims || !codes || !out)))
+    return fail(c, TB_EINVAL, "null argument");
+  if (n_states == 0 || n_obs == 0) return TB_OK;
+  std::vector<int> idims((size_t)n_states * (n + 1));
+  for (int64_t st = 0; st < n_states; ++st)
+    for (int64_t s = 0; s <= n; ++s) {
+      const int64_t d = dims[st * (n + 1) + s];
+      if (d < 1 || d > cap) return fail(c, TB_EINVAL, "bond dimension outside [1, cap]");
+      idims[(size_t)(st * (n + 1) + s)] = (int)d;
+    }
+  for (int64_t e = 0; e < n_obs * n; ++e)
+    if (codes[e] < 0 || codes[e] > 3) return fail(c, TB_EINVAL, "bad Pauli code");
+  const int grid = (int)(n_states < c->sms ? n_states : c->sms);
+  rc = ensure_workspace(c, grid, (int)n, (int)cap);
+  if (rc) return rc;
+  ++c->gen;  // the environments use the slot scratch
+  Staged sg;
+  double2* dbuf = sg.up((const double2*)bufs, (size_t)n_states * n * cap * 2 * cap);
+  int* dd = sg.up(idims.data(), idims.size());
+  int* dc = sg.up(codes, (size_t)(n_obs * n));
+  double* dout = sg.up<double>(nullptr, (size_t)(n_states * n_obs), false);
+  if (!dbuf || !dd || !dc || !dout) return fail(c, TB_ENOMEM, "device allocation failed");
+  const size_t smem = tb::kTileBytes;
+  TB_CUDA(c, cudaFuncSetAttribute(tb::expectation_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  tb::expectation_batch_kernel<<<grid, tb::NT, smem>>>(dbuf, (int)n_states, (int)n, (int)cap, dd, dc, (int)n_obs, c->W,
+                                                       c->W0, c->mat_stride, dout);
+  TB_CUDA(c, cudaGetLastError());
+  TB_CUDA(c, cudaMemcpy(out, dout, (size_t)(n_states * n_obs) * sizeof(double), cudaMemcpyDeviceToHost));
   return TB_OK;
 }
 

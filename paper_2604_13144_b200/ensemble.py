@@ -143,6 +143,13 @@ class EnsembleRun:
     extra: dict = field(default_factory=dict)
     excluded: np.ndarray | None = None  # [S] first checkpoint left out of the sums (-1: none)
     counts: np.ndarray | None = None    # [C] samples summed into each checkpoint row
+    states: np.ndarray | None = None    # complex128 [S, n, cap, 2, cap] final MPS per sample (retain_states)
+    state_dims: np.ndarray | None = None  # int32 [S, n+1]
+    state_center: np.ndarray | None = None  # int32 [S]
+    sample_ms: np.ndarray | None = None  # [S] device time per sample (time_samples)
+    sample_ids: np.ndarray | None = None
+    nu: np.ndarray | None = None         # [S] gate-list length per sample
+    signs: np.ndarray | None = None      # int8 [S, C] sign(g) of each prefix
 
     def row_counts(self) -> np.ndarray:
         """Samples that contributed to each checkpoint row of the sums."""
@@ -164,8 +171,12 @@ def excluded_counts(excluded: np.ndarray, n_ckpt: int) -> np.ndarray:
     return drop
 
 
-def run_packed(p: PackedEnsemble, device: int = 0, keep_values: bool = True) -> EnsembleRun:
-    """One end-to-end engine call with host buffers (``tb_run_ensemble``)."""
+def run_packed(p: PackedEnsemble, device: int = 0, keep_values: bool = True, retain_states: bool = False,
+               time_samples: bool = False) -> EnsembleRun:
+    """One end-to-end engine call with host buffers (``tb_run_ensemble``).
+    ``retain_states`` keeps every sample's final MPS (signed-mixture
+    post-processing, SPEC.md:413-417; memory n cap^2 per sample);
+    ``time_samples`` records each sample's device time (cost report)."""
     S, C, O = p.n_samples, p.ckpt_end.shape[1] if p.ckpt_end.ndim == 2 else 0, p.obs_sites.size
     values = np.zeros((S, C, O)) if keep_values else None
     disc = np.zeros((S, C)) if keep_values else None
@@ -176,6 +187,10 @@ def run_packed(p: PackedEnsemble, device: int = 0, keep_values: bool = True) -> 
     kms = np.zeros(1, np.float32)
     excl = np.full(S, -1, np.int32)
     check_row_capacity([S])
+    states = np.zeros((S, p.n, p.cap, 2, p.cap), np.complex128) if retain_states else None
+    sdims = np.zeros((S, p.n + 1), np.int32) if retain_states else None
+    scen = np.zeros(S, np.int32) if retain_states else None
+    sms = np.zeros(S) if time_samples else None
     arrays = [np.ascontiguousarray(x) for x in (p.words, p.offsets, p.ckpt_end, p.ckpt_sign, p.angle_cs,
                                                  p.weights, p.obs_sites, p.init_vecs)]
     w, off, ce, cs, ang, wt, obs, iv = arrays
@@ -186,24 +201,27 @@ def run_packed(p: PackedEnsemble, device: int = 0, keep_values: bool = True) -> 
                              p.init_dims.ctypes.data if p.init_dims is not None else None, p.init_center, 0)
     out = _lib.EnsembleOut(values.ctypes.data if values is not None else None,
                            disc.ctypes.data if disc is not None else None, ledger.ctypes.data,
-                           sv.ctypes.data, sv2.ctypes.data, flops.ctypes.data, kms.ctypes.data, excl.ctypes.data)
+                           sv.ctypes.data, sv2.ctypes.data, flops.ctypes.data, kms.ctypes.data, excl.ctypes.data,
+                           *(x.ctypes.data if x is not None else None for x in (states, sdims, scen, sms)))
     ctx = _lib.context(device)
     t0 = time.perf_counter()
     _lib.check(_lib.load().tb_run_ensemble(ctx, ctypes.byref(desc), ctypes.byref(out)), ctx)
     wall = time.perf_counter() - t0
     counts = S - excluded_counts(excl, C)
     return EnsembleRun(S, values, disc, ledger, sv, sv2, p.weights, float(flops[0]), float(kms[0]), wall,
-                       excluded=excl, counts=counts)
+                       excluded=excl, counts=counts, states=states, state_dims=sdims, state_center=scen,
+                       sample_ms=sms, sample_ids=p.sample_ids, nu=p.nu, signs=p.ckpt_sign)
 
 
 def run_ensemble(ham: Hamiltonian, cfg: PaiConfig, seed: int, sample_ids, init_labels, policy: TruncationPolicy,
                  checkpoints, observables=None, pi_local: bool = True, device: int = 0,
-                 keep_values: bool = True, init_state=None) -> EnsembleRun:
+                 keep_values: bool = True, init_state=None, retain_states: bool = False,
+                 time_samples: bool = False) -> EnsembleRun:
     """Batched ensemble: <Z_j> at each checkpoint step for every sample, plus the
     signed fixed-point sums of the estimator."""
     p = pack_ensemble(ham, cfg, seed, sample_ids, init_labels, policy, checkpoints, observables, pi_local,
                       init_state)
-    return run_packed(p, device, keep_values)
+    return run_packed(p, device, keep_values, retain_states, time_samples)
 
 
 def broadcast_state(state, src: int = 0, group=None):
@@ -469,8 +487,10 @@ class SlotPipeline:
             self.excluded.setdefault(sid, int(plan.sum_row[b, 0]))
         self.completed += plan.completes
 
-    def step_host(self, plan: StepPlan, values: np.ndarray | None = None) -> float:
-        """End-to-end step through ``tb_step`` with host buffers; returns kernel ms."""
+    def step_host(self, plan: StepPlan, values: np.ndarray | None = None, discarded: np.ndarray | None = None) -> float:
+        """End-to-end step through ``tb_step`` with host buffers; returns kernel ms.
+        ``values`` [S, 1, O] receives each slot's <Z_j>, ``discarded`` [S, 1]
+        its circuit's cumulative discarded weight at this checkpoint."""
         S, O = self.n_slots, self.proto.obs_sites.size
         check_row_capacity(self.row_count + 1)
         if self.step_engine is not None:
@@ -495,8 +515,9 @@ class SlotPipeline:
         flops = np.zeros(1)
         kms = np.zeros(1, np.float32)
         excl = np.full(S, -1, np.int32)
-        out = _lib.EnsembleOut(vals.ctypes.data, None, None, self.sum_v.ctypes.data, self.sum_v2.ctypes.data,
-                               flops.ctypes.data, kms.ctypes.data, excl.ctypes.data)
+        out = _lib.EnsembleOut(vals.ctypes.data, discarded.ctypes.data if discarded is not None else None, None,
+                               self.sum_v.ctypes.data, self.sum_v2.ctypes.data, flops.ctypes.data, kms.ctypes.data,
+                               excl.ctypes.data)
         _lib.check(_lib.load().tb_step(self.ctx, ctypes.byref(desc), ctypes.byref(out), self.sum_v.shape[0]), self.ctx)
         self.flops += float(flops[0])
         self._commit(plan, excl)

@@ -131,3 +131,101 @@ def results_table(times, stats: dict, g_norm, site: int, mean_nu=0.0, mean_cost=
             float(stats["var_o"][c, site]), float(stats["var_v"][c, site]), float(g_norm[c]),
             float(mean_nu), float(mean_cost), int(chi_max))))
     return "\n".join(lines) + "\n"
+
+
+# ---------------------------------------------------------------------------
+# Signed mixture (PAPER §II.C): rho(t) is the
+# Gamma-weighted signed average of the retained per-sample states, so any
+# observable is extracted in one pass over them, without re-simulation.
+# ---------------------------------------------------------------------------
+@dataclass
+class SignedMixture:
+    """(sign, MPS snapshot) pairs with the shared scale ||g||_1 / N_s."""
+
+    signs: np.ndarray        # int [S], sign(g_l) of each sample at the mixture's time
+    weight_norm: float       # ||g||_1 at that time (common to the ensemble)
+    states: np.ndarray       # complex128 [S, n, cap, 2, cap]
+    dims: np.ndarray         # int [S, n+1]
+    sample_ids: np.ndarray | None = None
+
+    @property
+    def n_samples(self) -> int:
+        return int(self.signs.size)
+
+    @property
+    def scale(self) -> float:
+        return self.weight_norm / self.n_samples
+
+
+def mixture_from_run(run) -> SignedMixture:
+    """The signed mixture of an ``EnsembleRun`` made with ``retain_states=True``:
+    the final states, each sample's sign at the last checkpoint, and the last
+    checkpoint's ||g||_1."""
+    if run.states is None:
+        raise ValueError("snapshots not retained: run the ensemble with retain_states=True")
+    if run.signs is None or run.signs.shape[1] == 0:
+        raise ValueError("the run has no checkpoint to attach the mixture to")
+    return SignedMixture(np.asarray(run.signs[:, -1], dtype=np.int64), float(run.weights[-1]), run.states,
+                         run.state_dims.astype(np.int64), run.sample_ids)
+
+
+def _codes(pauli, n: int) -> np.ndarray:
+    sym = {"X": 1, "Y": 2, "Z": 3}
+    c = np.zeros(n, np.int32)
+    for site, s in pauli.ops:
+        c[site] = sym[s]
+    return c
+
+
+def per_sample_expectations(mixture: SignedMixture, observables, device: int = 0) -> np.ndarray:
+    """<psi_l|P_o|psi_l> for every retained state and observable, [S, O]
+    (one batched engine call, ``tb_expectation_batch``)."""
+    import ctypes  # noqa: F401  (ctypes pointers through _lib)
+
+    from . import _lib
+
+    S, n, cap = mixture.states.shape[0], mixture.states.shape[1], mixture.states.shape[2]
+    obs = list(observables)
+    for o in obs:
+        if o.n != n:
+            raise ValueError("observable qubit count differs from the mixture's states")
+    codes = np.ascontiguousarray(np.stack([_codes(o, n) for o in obs]) if obs else np.zeros((0, n), np.int32))
+    out = np.zeros((S, len(obs)))
+    bufs = np.ascontiguousarray(mixture.states)
+    dims = np.ascontiguousarray(mixture.dims, dtype=np.int64)
+    ctx = _lib.context(device)
+    _lib.check(_lib.load().tb_expectation_batch(ctx, bufs.ctypes.data, S, n, cap, dims.ctypes.data, codes.ctypes.data,
+                                                len(obs), out.ctypes.data), ctx)
+    return out
+
+
+def evaluate_observables(mixture: SignedMixture, observables, device: int = 0) -> list:
+    """Tr[O rho(t)] = (||g||_1 / N_s) sum_l sign_l <psi_l|O|psi_l> for each
+    observable: equal to ``aggregate`` of that observable
+    computed sample-wise."""
+    if mixture.states is None:
+        raise ValueError("snapshots not retained")
+    vals = per_sample_expectations(mixture, observables, device)
+    return [float(x) for x in mixture.scale * (mixture.signs[:, None] * vals).sum(axis=0)]
+
+
+def variance_vs_bound_trace(times, stats: dict, g_norm, site: int = 0, n_samples=None, slack: float | None = None):
+    """Rows (t, Var[o], ||g||_1^2, Var[v]) per time (Fig. 4b):
+    asserts Var[o] <= ||g||_1^2 (1 + slack) at every t — |v| <= 1 bounds
+    Var[v] by N_s / (N_s - 1) for the unbiased sample variance, which is the
+    default slack."""
+    g = np.asarray(g_norm, dtype=np.float64)
+    rows = []
+    for c, t in enumerate(times):
+        var_o = float(stats["var_o"][c, site])
+        var_v = float(stats["var_v"][c, site])
+        bound = float(g[c] ** 2)
+        if slack is None:
+            ns = n_samples if n_samples is None or np.ndim(n_samples) == 0 else n_samples[c]
+            sl = (1.0 / (ns - 1) if ns and ns > 1 else 0.0) + 1e-12
+        else:
+            sl = slack
+        if var_o > bound * (1.0 + sl):
+            raise AssertionError(f"Var[o]={var_o} exceeds ||g||^2={bound} at t={t}")
+        rows.append((float(t), var_o, bound, var_v))
+    return rows

@@ -53,10 +53,16 @@ CONFIGS = {
 N_CKPT, EVERY = 20, 10
 
 
-def _install_gesvd():
-    """Swap the reference kernel's ``np.linalg.svd`` for zgesvd (this process only)."""
+def _select_driver(driver: str):
+    """Point the reference kernel's ``np`` at numpy itself (gesdd, as shipped)
+    or at a shim whose ``linalg.svd`` is zgesvd.  Called for EVERY job: pool
+    workers are reused, so the choice must never leak into the next job."""
     import scipy.linalg
     from tepai import _kernel
+
+    if driver == "gesdd":
+        _kernel.np = np
+        return
 
     def svd(a, full_matrices=True):
         return scipy.linalg.svd(a, full_matrices=full_matrices, lapack_driver="gesvd", check_finite=False)
@@ -72,9 +78,10 @@ def run_member(args):
     if os.path.exists(path):
         return path
     import tepai
+    from tepai import _kernel
     from tepai import rng as trng
-    if driver == "gesvd":
-        _install_gesvd()
+    _select_driver(driver)
+    assert (_kernel.np is np) == (driver == "gesdd")
     n, hs, cs, steps, T, chi, _ = CONFIGS[name]
     ham = tepai.build_spin_ring(n, 1.0, hs)
     circ = tepai.sample_circuit(ham, tepai.PaiConfig(DELTA, steps, T), trng.circuit_stream(cs, sid), sample_id=sid)
@@ -104,6 +111,20 @@ def run_member(args):
     return path
 
 
+def purge_leaked(names):
+    """Drop cached gesdd results that are bit-identical to their gesvd twin at
+    the last checkpoint (made by an earlier version of this script whose
+    workers kept the zgesvd shim installed); they are recomputed."""
+    for nm in names:
+        for i in range(CONFIGS[nm][6]):
+            a = os.path.join(CACHE, f"{nm}_gesdd_{i}.npz")
+            b = os.path.join(CACHE, f"{nm}_gesvd_{i}.npz")
+            if os.path.exists(a) and os.path.exists(b):
+                va, vb = np.load(a)["vals"], np.load(b)["vals"]
+                if np.array_equal(va[-1], vb[-1]):
+                    os.remove(a)
+
+
 def assemble(name):
     import tepai
     n, hs, cs, steps, T, chi, count = CONFIGS[name]
@@ -127,11 +148,16 @@ def main():
     ap.add_argument("--procs", type=int, default=max(1, (os.cpu_count() or 2) - 1))
     ap.add_argument("--only", choices=sorted(CONFIGS), default=None)
     a = ap.parse_args()
-    names = [a.only] if a.only else ["c3", "c2"]
+    names = [a.only] if a.only else ["c2", "c3"]
+    purge_leaked(names)
     jobs = [(nm, i, d) for nm in names for i in range(CONFIGS[nm][6]) for d in ("gesdd", "gesvd")]
     with Pool(a.procs) as pool:
         for k, p in enumerate(pool.imap_unordered(run_member, jobs, chunksize=1)):
             print(f"[{k + 1}/{len(jobs)}] {os.path.basename(p)}", flush=True)
+    purge_leaked(names)
+    missing = [j for j in jobs if not os.path.exists(os.path.join(CACHE, f"{j[0]}_{j[2]}_{j[1]}.npz"))]
+    if missing:
+        raise SystemExit(f"{len(missing)} results were purged as driver leaks; run the script again")
     for nm in names:
         assemble(nm)
     print("written:", [f"ref_{nm}_stat.npz" for nm in names])

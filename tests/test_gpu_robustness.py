@@ -22,22 +22,27 @@ def _c1():
 
 
 def test_nonconverged_samples_are_excluded_not_fatal(engine, monkeypatch):
-    ham, cfg, ck = _c1()
-    monkeypatch.setenv("TB_MAX_SWEEPS", "1")  # force Jacobi non-convergence (test hook)
-    run = tb.run_ensemble(ham, cfg, 1, range(24), "01" * 4, tb.TruncationPolicy(16), ck)
+    # C2-shaped prefix (64 x 64 preconditioned problems); a one-sweep cap on the
+    # Jacobi (test hook) leaves many of them unconverged
+    ham = tb.build_spin_ring(16, 1.0, 2)
+    cfg = tb.PaiConfig(DELTA, 30, 0.3)
+    ck = np.array([10, 20, 30])
+    pol = tb.TruncationPolicy(32, 1e-12)
+    monkeypatch.setenv("TB_MAX_SWEEPS", "1")
+    run = tb.run_ensemble(ham, cfg, 3, range(24), "01" * 8, pol, ck)
     ex = run.excluded
     assert ex is not None and np.any(ex >= 0)
     counts = run.row_counts()
     np.testing.assert_array_equal(counts, 24 - ensemble.excluded_counts(ex, ck.size))
     # the sums hold exactly the checkpoints before each sample's exclusion point
-    p = ensemble.pack_ensemble(ham, cfg, 1, range(24), "01" * 4, tb.TruncationPolicy(16), ck)
+    p = ensemble.pack_ensemble(ham, cfg, 3, range(24), "01" * 8, pol, ck)
     want = np.zeros_like(run.sum_v)
     for s in range(24):
         stop = ck.size if ex[s] < 0 else ex[s]
         want[:stop] += quantize(p.ckpt_sign[s, :stop, None] * run.values[s, :stop])
     np.testing.assert_array_equal(run.sum_v, want)
     # without the exclusion array the launch fails and the caller's arrays stay untouched
-    S, C, O = 24, ck.size, 8
+    S, C, O = 24, ck.size, 16
     sv = np.full((C, O), 7, np.int64)
     sv2 = np.full((C, O), 7, np.int64)
     flops = np.zeros(1)

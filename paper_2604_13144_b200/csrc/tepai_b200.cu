@@ -78,6 +78,7 @@ struct Job {
   int n, cap, chi_cut, pi_local;
   int precond;  // QR-preconditioned Jacobi for problems >= 32 x 32
   int max_sweeps;  // Jacobi sweep cap (TB_MAX_SWEEPS, tests of the non-convergence path only)
+  int inject;      // fault injection (TB_FAULT_INJECT=k): every Jacobi of samples with id % k == 0 reports non-convergence
   int tail_skip;  // skip pairs of discarded-tail columns (see mark_tail)
   int qrcp_tmem;  // QR preconditioner with the matrix in tensor memory (qrcp_tmem)
   double floor;
@@ -151,6 +152,7 @@ struct Smem {
   int flag;
   int bad;                   // this sample hit a non-converged SVD: its later checkpoints stay out of the sums
   int maxsweep;              // Jacobi sweep cap (MAXSWEEP; lowered only by the failure-path tests)
+  int inject;                // fault injection period (samples with index % inject == 0)
   int sweeps;
   int rotcount;
   uint32_t tmem;             // TMEM base address (512 columns, allocated per CTA)
@@ -459,7 +461,14 @@ __device__ void sort_sigma(const double2* W, int Mw, int Nw, Smem& sm) {
   __syncthreads();
 }
 
-__device__ __forceinline__ long long prof_clock() { return clock64(); }
+// Phase profiling (clock64 counters summed into Job::prof) is compiled in only
+// for diagnostics builds (-DTB_PROF=1, libtepai_b200_prof.so, used by tools/);
+// the product library has no clock reads, no profiling atomics and no
+// registers held for them in the hot loops.
+#ifndef TB_PROF
+#define TB_PROF 0
+#endif
+__device__ __forceinline__ long long prof_clock() { return TB_PROF ? clock64() : 0ll; }
 // per-step clocks inside the QRCP loop: a clock64 read per sub-phase costs a
 // few % of the loop, so they are compiled in only for phase studies
 #ifndef TB_PHASE_CLOCKS
@@ -487,23 +496,33 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
 
-// Rotation of one pair.  Identity when s == 0 (c = 1, e = 1).
+// Rotation of one pair in the "tau" form.  With g = a^H b, d = beta - alpha,
+// the Jacobi angle is t = 2|g| sgn(d) / (|d| + sqrt(d^2 + 4|g|^2)) and the
+// unitary update a' = c (a - t e b), b' = c (b + t conj(e) a), e = conj(g)/|g|,
+// c = 1/sqrt(1+t^2).  Writing t e = tau conj(g) with
+//   tau = t / |g| = 2 sgn(d) / (|d| + sqrt(d^2 + 4|g|^2))
+// removes the normalisation of e (a full-precision rsqrt) from the chain, and
+// c = 1/sqrt(1 + tau^2 |g|^2) keeps the transform EXACTLY unitary for any tau:
+// tau only sets the angle, so it is evaluated from the MUFU seeds alone
+// (~2^-21 relative; the pair's coupling then drops to ~5e-7 of its value
+// instead of to rounding, far below the sweep's quadratic rate).  c needs
+// full precision (it enters the column scales) and gets two Newton steps.
+// About 20 fewer FP64 instructions per pair and half the dependency depth of
+// the former (t, c, e) evaluation — the scalar parameter math, executed by
+// all 16 lanes of a half, was half of the FP64 pipe's busy time (r02a ncu:
+// DMUL 13.2e12 vs DFMA 26.1e12 thread instructions).
 struct Rot {
-  double c, s, er, ei, tg, t;
+  double c, tau, tg, g2;
+  bool rot;
 };
 __device__ __forceinline__ void atomic_max_pos(double* a, double v) {  // v >= 0
   atomicMax((unsigned long long*)a, (unsigned long long)__double_as_longlong(v));
 }
 
-// Jacobi parameters for one pair (alpha = |a|^2, beta = |b|^2, g = a^H b):
-// t = 2|g| sgn(d) / (|d| + sqrt(d^2 + 4|g|^2)), d = beta - alpha (the smaller
-// root of t^2 + 2 zeta t - 1 = 0), c = 1/sqrt(1+t^2), s = t c, e = conj(g)/|g|.
 // A pair is left alone when it is orthogonal to relative precision
-// (|g|^2 <= tol2 alpha beta) or when the rotation would move either column by
-// less than the absolute rounding floor of the matrix (|g|^2 <= abs2 *
-// max(alpha, beta)) — the same absolute accuracy LAPACK's SVD delivers.
-// Branch-free FP64 reciprocal square root / reciprocal for well-scaled
-// positive arguments: MUFU seed + Newton steps (2 steps: ~1 ulp).
+// (|g|^2 <= tol2 alpha beta); it then gets tau = 0 and c = 1 (the exact identity).
+// Branch-free FP64 reciprocal square root for well-scaled positive
+// arguments: MUFU seed + Newton steps (2 steps: ~1 ulp).
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -512,41 +531,19 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   y = y * fma(-h * y, y, 1.5);
   return y;
 }
-__device__ __forceinline__ double rsqrt_nr1(double x) {  // one Newton step: ~2^-44 relative
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  return y * fma(-0.5 * x * y, y, 1.5);
-}
-__device__ __forceinline__ double rcp_nr1(double x) {  // ~2^-44 relative
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  y = y * fma(-x, y, 2.0);
-  return y;
-}
 
 __device__ __forceinline__ Rot rot_params(double gr, double gi, double al, double be, bool valid, double tol2) {
   Rot p;
-  const double g2 = fma(gr, gr, gi * gi);
-  const bool rot = valid && (g2 > tol2 * al * be);
-  // t only fixes the rotation angle (an approximate t still gives an exactly
-  // unitary rotation, c = 1/sqrt(1+t^2), s = t c); c and e = conj(g)/|g| are
-  // evaluated to full precision.
-  const double gs = rot ? g2 : 1.0;
-  const double ig = rsqrt_nr(gs);
-  const double g = gs * ig;
+  p.g2 = fma(gr, gr, gi * gi);
+  p.rot = valid && (p.g2 > tol2 * al * be);
   const double d = be - al;
-  const double h2 = fma(d, d, 4.0 * gs);
-  const double h = h2 * rsqrt_nr1(h2);  // only fixes the angle t (see above)
-  // a pair left alone gets t = 0 and c = 1 (the exact identity: s, tg and the
-  // scaled factors built from t vanish; e stays finite because gs = 1)
-  const double t = rot ? copysign(2.0 * g, d) * rcp_nr1(fabs(d) + h) : 0.0;
-  const double c = rsqrt_nr(fma(t, t, 1.0));
-  p.c = rot ? c : 1.0;
-  p.s = t * c;
-  p.er = gr * ig;
-  p.ei = -gi * ig;
-  p.tg = t * g;
-  p.t = t;
+  const double h2 = p.rot ? fma(d, d, 4.0 * p.g2) : 1.0;
+  double y, r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h2));
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(fabs(d) + h2 * y));
+  p.tau = p.rot ? copysign(2.0, d) * r : 0.0;
+  p.c = p.rot ? rsqrt_nr(fma(p.tau * p.tau, p.g2, 1.0)) : 1.0;
+  p.tg = p.tau * p.g2;  // t |g|: the exact norm transfer alpha' = alpha - t|g|, beta' = beta + t|g|
   return p;
 }
 
@@ -637,6 +634,35 @@ __device__ __forceinline__ double half_sum(double v) {
   v += __shfl_xor_sync(0xffffffffu, v, 2);
   v += __shfl_xor_sync(0xffffffffu, v, 1);
   return v;
+}
+
+// Sum of eight values over the 16 lanes of each half-warp, returned to every
+// lane of the half: a transposed reduction (8 + 4 + 2 + 1 lane-pair exchanges
+// keep halving the values each lane carries, the last step pairs lanes l and
+// l ^ 1) and one broadcast shuffle per value — 16 double shuffles instead of
+// the 32 of eight separate butterflies, in one dependency chain instead of eight.
+__device__ __forceinline__ void half_sum8(double (&v)[8]) {
+  const unsigned full = 0xffffffffu;
+  const int l = threadIdx.x & 15;
+  const bool b3 = l & 8, b2 = l & 4, b1 = l & 2;
+  double a[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double send = b3 ? v[k] : v[k + 4], keep = b3 ? v[k + 4] : v[k];
+    a[k] = keep + __shfl_xor_sync(full, send, 8);
+  }
+  double b[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double send = b2 ? a[k] : a[k + 2], keep = b2 ? a[k + 2] : a[k];
+    b[k] = keep + __shfl_xor_sync(full, send, 4);
+  }
+  double c = (b1 ? b[1] : b[0]) + __shfl_xor_sync(full, b1 ? b[0] : b[1], 2);
+  c += __shfl_xor_sync(full, c, 1);
+  // value k now sits on lanes 2k and 2k + 1 of the half (bits 3..1 of the lane)
+  const int base = threadIdx.x & 16;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = __shfl_sync(full, c, base | (2 * k));
 }
 
 constexpr double kTailTol2 = 1e-8;  // (relative coupling 1e-4)^2 for pairs of two tail columns
@@ -748,17 +774,18 @@ __device__ __forceinline__ bool rot_half(HCol<HR>& a, const HCol<HR>& b, uint32_
   gr *= dd;
   gi *= dd;
   const Rot p = rot_params(gr, gi, na, nb, valid, tol2);
-  const bool mine = p.s != 0.0;
+  const bool mine = p.rot;
   if (mine) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(na * nb));
-    offmax = fmax(offmax, fma(gr, gr, gi * gi) * r);
+    offmax = fmax(offmax, p.g2 * r);
   }
   const double nan_ = na - p.tg, nbn = nb + p.tg;
   if (__any_sync(0xffffffffu, mine)) {
+    // f1 = t e db/da = tau conj(g) db/da, f2 = t conj(e) da/db = tau g da/db
     const double inv = rcp_acc(dd);
-    const double r1 = p.t * db * db * inv, r2 = p.t * da * da * inv;
-    apply_rot_s<HR, KEEP_A>(a, b, sa, sb, mine, p.er * r1, p.ei * r1, p.er * r2, -p.ei * r2);
+    const double r1 = p.tau * db * db * inv, r2 = p.tau * da * da * inv;
+    apply_rot_s<HR, KEEP_A>(a, b, sa, sb, mine, gr * r1, -gi * r1, gr * r2, gi * r2);
     da *= p.c;
     db *= p.c;
   }
@@ -903,7 +930,7 @@ struct JacobiH {
     }
     __syncthreads();
     if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
-    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[14], (unsigned long long)(prof_clock() - tc0));
+    if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[14], (unsigned long long)(prof_clock() - tc0));
   }
 
   __device__ void load_p(HCol<HR>& pc, double& np, double& dp, int s, Smem& sm) {
@@ -1017,7 +1044,7 @@ struct JacobiH {
     const int nsm = min(nblk, 3);
     const long long tw0 = prof_clock();
     within(0, 1, 2, nsm, sm);
-    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[13], (unsigned long long)(prof_clock() - tw0));
+    if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[13], (unsigned long long)(prof_clock() - tw0));
     HCol<HR> pc;
     double np, dp;
     if (nblk == 4) {
@@ -1046,7 +1073,7 @@ struct JacobiH {
         }
         __syncthreads();
       }
-      if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[27], (unsigned long long)(prof_clock() - tsw));
+      if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[27], (unsigned long long)(prof_clock() - tsw));
       within(0, 0, 0, 1, sm);
       load_p(pc, np, dp, 3, sm);
       cross(pc, np, dp, sm.jncol[3], 3, 1, 2, 2, 2, sm);
@@ -1092,15 +1119,15 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16 * TB_TOLSCALE;
   const int nsm = min(J.nblk, 3);
   if (J.nblk == 4) {
-    double2 tmp[(JB * 128 + NT - 1) / NT];
-    int cnt = 0;
-    for (int e = threadIdx.x; e < JB * Mw; e += NT, ++cnt) {
+    // block 3 moves to G (columns 96..127 of W), overlapping its source
+    // columns: bounce it through the not yet filled shared-memory slots
+    for (int e = threadIdx.x; e < JB * Mw; e += NT) {
       const int k = e / Mw, y = e - k * Mw;
-      tmp[cnt] = (k < ncl[3]) ? W[(size_t)(start[3] + k) * Mw + y] : cz();
+      smem[e] = (k < ncl[3]) ? W[(size_t)(start[3] + k) * Mw + y] : cz();
     }
     __syncthreads();
-    cnt = 0;
-    for (int e = threadIdx.x; e < JB * Mw; e += NT, ++cnt) J.G[e] = tmp[cnt];
+    for (int e = threadIdx.x; e < JB * Mw; e += NT) J.G[e] = smem[e];
+    __syncthreads();
   }
   for (int e = threadIdx.x; e < nsm * JB * LD; e += NT) {
     const int c = e / LD, y = e - c * LD;
@@ -1108,7 +1135,7 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     smem[e] = (k < ncl[sb] && y < Mw) ? W[(size_t)(start[sb] + k) * Mw + y] : cz();
   }
   __syncthreads();
-  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[25], (unsigned long long)(prof_clock() - tj0));
+  if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[25], (unsigned long long)(prof_clock() - tj0));
   auto live = [&](int c) { return (c & (JB - 1)) < sm.jncol[c / JB]; };
   if (threadIdx.x == 0) sm.ntail = 0;
   int sweep = 0;
@@ -1117,10 +1144,10 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     const long long ts0 = prof_clock();
     J.refresh_norms(sm, tol, sweep == 0);
     if (sweep == 1) mark_tail(sm, JB * J.nblk, live);
-    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[26], (unsigned long long)(prof_clock() - ts0));
+    if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[26], (unsigned long long)(prof_clock() - ts0));
     J.sweep(sm);
     __syncthreads();
-    if (threadIdx.x == 0 && sm.prof && Mw == 128 && sweep < 16) {
+    if (threadIdx.x == 0 && TB_PROF && sm.prof && Mw == 128 && sweep < 16) {
       atomicAdd(&sm.prof[40 + sweep], (unsigned long long)(prof_clock() - ts0));
       atomicAdd(&sm.prof[56 + min(sweep, 7)], 1ull);
     }
@@ -1139,7 +1166,7 @@ __device__ int jacobi_half(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
     W[(size_t)c * Mw + y] = smem[(size_t)c * LD + y];
   }
   __syncthreads();
-  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[28], (unsigned long long)(prof_clock() - tw0));
+  if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[28], (unsigned long long)(prof_clock() - tw0));
   const int neff = (J.nblk == 1) ? Nw : JB * J.nblk;
   return conv ? neff : -neff;
 }
@@ -1213,17 +1240,17 @@ struct JacobiW {
     gr *= dd;
     gi *= dd;
     const Rot p = rot_params(gr, gi, na, nb, valid, tl2);
-    const bool mine = p.s != 0.0;
+    const bool mine = p.rot;
     if (mine) {
       double r;
       asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(na * nb));
-      offmax = fmax(offmax, fma(gr, gr, gi * gi) * r);
+      offmax = fmax(offmax, p.g2 * r);
     }
     const double nan_ = na - p.tg, nbn = nb + p.tg;
     if (__any_sync(0xffffffffu, mine)) {
       const double inv = rcp_acc(dd);
-      const double r1 = p.t * db * db * inv, r2 = p.t * da * da * inv;
-      const double f1r = p.er * r1, f1i = p.ei * r1, f2r = p.er * r2, f2i = -p.ei * r2;
+      const double r1 = p.tau * db * db * inv, r2 = p.tau * da * da * inv;
+      const double f1r = gr * r1, f1i = -gi * r1, f2r = gr * r2, f2i = gi * r2;
 #pragma unroll
       for (int q0 = 0; q0 < HR; q0 += CH) {
 #pragma unroll
@@ -1485,6 +1512,8 @@ __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* 
     const int sw = hestenes(W, Mw, Nw, sm);
     neff = (sw > MAXSWEEP) ? -Nw : Nw;
   }
+  // fault injection (tests of the exclusion path): a CTA-uniform decision
+  if (sm.inject > 0 && sm.sample % sm.inject == 0 && neff > 0) neff = -neff;
   if (neff < 0) {
     if (threadIdx.x == 0) {
       atomicOr(status, 1);
@@ -1682,7 +1711,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     tqd += tt4 - tt3;
     tq1 += prof_fine() - tt4;
   }
-  if (threadIdx.x == 0 && sm.prof) {
+  if (threadIdx.x == 0 && TB_PROF && sm.prof) {
     atomicAdd(&sm.prof[15], (unsigned long long)j);
     atomicAdd(&sm.prof[32], (unsigned long long)tqa);   // pivot selection
     atomicAdd(&sm.prof[33], (unsigned long long)tqb);   // register-pivot publication (incl. its barrier)
@@ -1879,17 +1908,33 @@ __device__ __noinline__ int qrcp_tmem(const double2* Y, int Nw, int Mw, double2*
         R[(size_t)j * Mw + c] = d;
       }
     };
-#pragma unroll 1
+    // Two passes over the half's four columns: every dot product first
+    // (partial sums only), ONE transposed reduction of the eight partials,
+    // then the updates, re-reading each column from tensor memory (which
+    // streams far faster than the reductions' latency) instead of holding
+    // it.  The four per-column reduction chains no longer serialise.
+    bool vt[4];
+    double part[8];
+#pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int c = hw + 32 * t;
-      const bool valid = c < Mw && c != p && sm.nrm[c] >= 0.0;
-      if (!__any_sync(0xffffffffu, valid)) continue;
+      vt[t] = c < Mw && c != p && sm.nrm[c] >= 0.0;
+      double2 d = cz();
+      if (__any_sync(0xffffffffu, vt[t])) {
+        HCol<HR> y;
+        tm_ld_col(tcol + 32u * t, y);
+        d = dotp(y);
+      }
+      part[2 * t] = d.x;
+      part[2 * t + 1] = d.y;
+    }
+    half_sum8(part);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (!__any_sync(0xffffffffu, vt[t])) continue;
       HCol<HR> y;
       tm_ld_col(tcol + 32u * t, y);
-      double2 d = dotp(y);
-      d.x = half_sum(d.x);
-      d.y = half_sum(d.y);
-      apply(y, c, valid, d);
+      apply(y, hw + 32 * t, vt[t], make_double2(part[2 * t], part[2 * t + 1]));
       tm_st_col(tcol + 32u * t, y);
     }
     tm_wait_st();
@@ -1898,7 +1943,7 @@ __device__ __noinline__ int qrcp_tmem(const double2* Y, int Nw, int Mw, double2*
     local_best();
     __syncthreads();
   }
-  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
+  if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
   // complete the permutation with the numerically dead columns
   if (threadIdx.x == 0) {
     int k = j;
@@ -1924,7 +1969,7 @@ template <int HR>
 __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
   const long long t0 = prof_clock();
   const int r = (sm.tmem_on && HR == 8) ? qrcp_tmem(W, Nw, Mw, X, sm, smem) : qrcp_mgs<HR>(W, Nw, Mw, X, sm, smem);
-  if (threadIdx.x == 0 && sm.prof) {
+  if (threadIdx.x == 0 && TB_PROF && sm.prof) {
     atomicAdd(&sm.prof[12], (unsigned long long)(prof_clock() - t0));
     atomicAdd(&sm.prof[8], 1ull);
   }
@@ -1933,7 +1978,7 @@ __device__ int precond_jacobi_t(double2* W, double2* X, int Mw, int Nw, Smem& sm
   if (r > 0) {
     const long long tb0 = prof_clock();
     build_l(X, Mw, r, W, sm);
-    if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[24], (unsigned long long)(prof_clock() - tb0));
+    if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[24], (unsigned long long)(prof_clock() - tb0));
     neff = jacobi(W, Mw, r, sm, smem, status);
   }
   // the numerically dead directions are exact zero columns
@@ -2076,7 +2121,7 @@ __device__ int qrcp_wide(double2* Y, int Nw, int Mw, double2* R, Smem& sm, doubl
     local_best();
     __syncthreads();
   }
-  if (threadIdx.x == 0 && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
+  if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[15], (unsigned long long)j);
   if (threadIdx.x == 0) {
     int k = j;
     for (int c = 0; c < Mw; ++c)
@@ -2090,7 +2135,7 @@ __device__ int qrcp_wide(double2* Y, int Nw, int Mw, double2* R, Smem& sm, doubl
 __device__ int precond_jacobi_wide(double2* W, double2* X, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
   const long long t0 = prof_clock();
   const int r = qrcp_wide(W, Nw, Mw, X, sm, smem);
-  if (threadIdx.x == 0 && sm.prof) {
+  if (threadIdx.x == 0 && TB_PROF && sm.prof) {
     atomicAdd(&sm.prof[12], (unsigned long long)(prof_clock() - t0));
     atomicAdd(&sm.prof[8], 1ull);
   }
@@ -2119,7 +2164,7 @@ __device__ int precond_jacobi(double2* W, double2* X, int Mw, int Nw, Smem& sm, 
 // Per-CTA sample context
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ void prof_add(const Job& jb, int slot, long long v) {
-  if (threadIdx.x == 0 && jb.prof) atomicAdd(&jb.prof[slot], (unsigned long long)v);
+  if (TB_PROF && threadIdx.x == 0 && jb.prof) atomicAdd(&jb.prof[slot], (unsigned long long)v);
 }
 
 constexpr int kTileElems = 2 * TK * TLD;                                // GEMM staging tiles
@@ -2633,7 +2678,9 @@ __device__ void record_checkpoint(const Ctx& cx, Smem& sm, int sample, int ck) {
   // contributes nothing from that checkpoint on; the caller learns which
   // checkpoint through `excluded` and drops it from that row's count
   const bool bad = sm.bad != 0;
-  if (bad && threadIdx.x == 0 && jb.excluded) atomicMin(&jb.excluded[sample], ck);
+  // (one CTA owns the sample and records its checkpoints in order: the first
+  // excluded checkpoint is the first write over the caller's -1)
+  if (bad && threadIdx.x == 0 && jb.excluded && jb.excluded[sample] < 0) jb.excluded[sample] = ck;
   for (int o = threadIdx.x; o < jb.n_obs; o += NT) {
     const double z = sm.zval[jb.obs_sites[o]];
     if (jb.values) jb.values[((size_t)sample * jb.n_ckpt + ck) * jb.n_obs + o] = z;
@@ -2670,6 +2717,7 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
     sm.tmem_on = job.qrcp_tmem;
     sm.bad = 0;
     sm.maxsweep = job.max_sweeps;
+    sm.inject = job.inject;
   }
   if (job.qrcp_tmem) tmem_alloc(sm);
   for (int iter = 0;; ++iter) {
@@ -2924,6 +2972,8 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
     sm.kcut = (kcut > 0 && kcut < K) ? kcut : MAXDIM;
     sm.tmem_on = (precond >> 1) & 1;
     sm.maxsweep = MAXSWEEP;
+    sm.inject = 0;
+    sm.sample = 0;
   }
   if (precond & 2) tmem_alloc(sm);
   double2* W = Wg + mat_stride * b;
@@ -3127,6 +3177,8 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
     const char* ms = getenv("TB_MAX_SWEEPS");
     job.max_sweeps = ms ? atoi(ms) : tb::MAXSWEEP;
     if (job.max_sweeps < 1 || job.max_sweeps > tb::MAXSWEEP) job.max_sweeps = tb::MAXSWEEP;
+    const char* fi = getenv("TB_FAULT_INJECT");
+    job.inject = fi ? atoi(fi) : 0;
   }
   job.floor = d->svalue_floor;
   job.n_samples = d->n_samples;
@@ -3148,7 +3200,7 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
   job.sum_v = (unsigned long long*)o->sum_v;
   job.sum_v2 = (unsigned long long*)o->sum_v2;
   job.flops = c->dflops;
-  job.prof = c->profile ? c->dprof : nullptr;  // phase atomics only in diagnostic runs
+  job.prof = (TB_PROF && c->profile) ? c->dprof : nullptr;  // phase atomics only in diagnostics builds
   job.next_sample = c->dscratch;
   job.status = c->dscratch + 1;
   job.excluded = o->excluded;

@@ -22,16 +22,16 @@ def _c1():
 
 
 def test_nonconverged_samples_are_excluded_not_fatal(engine, monkeypatch):
-    # C2-shaped prefix (64 x 64 preconditioned problems); a one-sweep cap on the
-    # Jacobi (test hook) leaves many of them unconverged
+    # fault injection (test hook): every SVD of the samples with index % 5 == 0
+    # reports non-convergence
     ham = tb.build_spin_ring(16, 1.0, 2)
     cfg = tb.PaiConfig(DELTA, 30, 0.3)
     ck = np.array([10, 20, 30])
     pol = tb.TruncationPolicy(32, 1e-12)
-    monkeypatch.setenv("TB_MAX_SWEEPS", "1")
+    monkeypatch.setenv("TB_FAULT_INJECT", "5")
     run = tb.run_ensemble(ham, cfg, 3, range(24), "01" * 8, pol, ck)
     ex = run.excluded
-    assert ex is not None and np.any(ex >= 0)
+    np.testing.assert_array_equal(ex >= 0, np.arange(24) % 5 == 0)
     counts = run.row_counts()
     np.testing.assert_array_equal(counts, 24 - ensemble.excluded_counts(ex, ck.size))
     # the sums hold exactly the checkpoints before each sample's exclusion point

@@ -1,5 +1,6 @@
 """Cycle breakdown of the batched 128x128 SVD kernel (diagnostic counters)."""
-import os; os.environ.setdefault("TB_PROFILE", "1")  # phase counters are diagnostics-only
+import os, sys; sys.path.insert(0, "."); import __graft_entry__; __graft_entry__.build(profile=True)  # noqa: E702
+os.environ.setdefault("TB_PROFILE", "1"); os.environ.setdefault("TB_LIB", __graft_entry__.LIB_PROF)  # phase counters: diagnostics build
 import sys, numpy as np
 sys.path.insert(0, ".")
 from paper_2604_13144_b200 import _lib

@@ -1,7 +1,8 @@
 """Load balance of the slot-mode step (bench definition): per launch, kernel
 time vs the mean per-CTA busy time (clock64 counter prof[7] / CTAs / clock).
 usage: python tools/slot_balance.py [steps] [slots]"""
-import os; os.environ.setdefault("TB_PROFILE", "1")  # phase counters are diagnostics-only
+import os, sys; sys.path.insert(0, "."); import __graft_entry__; __graft_entry__.build(profile=True)  # noqa: E702
+os.environ.setdefault("TB_PROFILE", "1"); os.environ.setdefault("TB_LIB", __graft_entry__.LIB_PROF)  # phase counters: diagnostics build
 import math, sys
 import numpy as np
 sys.path.insert(0, ".")

@@ -1,6 +1,7 @@
 """Time the engine on a prefix of a config's circuits (exploration tool).
 usage: python tools/time_prefix.py N_SITES CHI HAM_SEED CIRC_SEED STEPS T N_SAMPLES MAX_STEP"""
-import os; os.environ.setdefault("TB_PROFILE", "1")  # phase counters are diagnostics-only
+import os, sys; sys.path.insert(0, "."); import __graft_entry__; __graft_entry__.build(profile=True)  # noqa: E702
+os.environ.setdefault("TB_PROFILE", "1"); os.environ.setdefault("TB_LIB", __graft_entry__.LIB_PROF)  # phase counters: diagnostics build
 import math, sys, time
 import numpy as np
 sys.path.insert(0, ".")

@@ -80,6 +80,8 @@ struct Job {
   int max_sweeps;  // Jacobi sweep cap (TB_MAX_SWEEPS, tests of the non-convergence path only)
   int inject;      // fault injection (TB_FAULT_INJECT=k): every Jacobi of samples with id % k == 0 reports non-convergence
   int tail_skip;  // skip pairs of discarded-tail columns (see mark_tail)
+  int cluster;    // CTAs per thread-block cluster (8: wide Jacobi in distributed smem; 0: none)
+  int cluster_tma;  // cluster Jacobi stages its blocks with TMA bulk copies
   int qrcp_tmem;  // QR preconditioner with the matrix in tensor memory (qrcp_tmem)
   double floor;
   int n_samples, n_ckpt, n_obs;
@@ -162,6 +164,19 @@ struct Smem {
   unsigned long long* prof;
   int sample;
   int center;
+  // cluster Jacobi (jacobi_cluster): command posted by the leader, reductions
+  int cluster;               // CTAs per cluster (0/1: no cluster)
+  int cl_op;                 // 1: Jacobi on (cl_W, cl_Mw, cl_Nw), 0: exit
+  double2* cl_W;
+  int cl_Mw, cl_Nw, cl_maxsweep;
+  int cl_flag[2];
+  double cl_off[2];
+  double cl_part[8];
+  int cl_rflag;
+  double cl_roff;
+  uint16_t cl_sched[16];
+  int cl_tma;                // stage the blocks with TMA bulk copies (else plain loads/stores)
+  unsigned long long cl_mbar;  // mbarrier of the bulk loads
 };
 
 // ----------------------------------------------------------------------------
@@ -1498,6 +1513,556 @@ __device__ int jacobi_wide(double2* W, int Mw, int Nw, Smem& sm, double2* smem) 
   return conv ? Nw : -Nw;
 }
 
+// ----------------------------------------------------------------------------
+// Cluster Jacobi: the chi = 128 problems (Mw <= 256 rows x Nw <= 256 columns,
+// 1 MB of complex128) held in the DISTRIBUTED shared memory of an 8-CTA
+// thread-block cluster instead of streaming through L2 (jacobi_wide).
+//
+// The columns form 16 blocks of <= 16; CTA r of the cluster homes blocks 2r
+// and 2r+1 in its shared memory (256 padded rows x 16 B = 4 KB per column,
+// 128 KB per CTA).  A sweep is
+//   * a within-block round robin of each CTA's two home blocks (warps 0-7 and
+//     8-15, one pair per warp per round), then
+//   * the 15 rounds of the circle method over the 16 blocks.  Each round is a
+//     perfect matching of the blocks; every CTA takes exactly ONE matched pair
+//     (X, Y) in which Y is one of its own home blocks (the matching, seen as a
+//     2-regular multigraph on the CTAs, is oriented along its cycles), loads
+//     the 16 columns of X into registers (one column per warp, 8 rows per lane)
+//     over DSMEM, rotates them against the 16 local columns of Y in 16 rounds
+//     (warp w: X_w against Y_(w+r) mod 16), and writes X back to its home CTA.
+// A column lives in one whole warp, so a pair's reductions are 5-level
+// butterflies and its rotation parameters need no broadcast.  Same scaled
+// (tau-form) rotations, pair skipping, dead-column rule and convergence test
+// as the single-CTA paths; the per-sweep flag / largest off-diagonal and the
+// Frobenius norm are reduced over the cluster in fixed rank order, so every
+// CTA takes the same branch and the result is deterministic.
+//
+// The leader CTA (rank 0) runs the whole circuit; ranks 1..7 wait in
+// cluster_follow() for a command posted through the leader's shared memory.
+// Replaces the zgesdd of /root/reference/pkg/src/tepai/_kernel.py:117 at
+// 2*chi = 256 (SURVEY.md §8 north_star (1)).
+// ----------------------------------------------------------------------------
+constexpr int CL = 8;            // CTAs per cluster
+constexpr int CNB = 2 * CL;      // column blocks
+constexpr int CBC = 16;          // max columns per block
+constexpr uint32_t CCB = 4096u;  // bytes per shared-memory column (256 rows)
+
+__device__ __forceinline__ int cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return (int)r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double2 ldc2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void stc2(uint32_t a, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double ldcf(uint32_t a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void stcf(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ldcu(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ldcl(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ldcb(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void stcb(uint32_t a, uint32_t v) {
+  asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// TMA bulk copies (cp.async.bulk) between global and shared memory, completed
+// through an mbarrier (global -> smem) or a bulk group (smem -> global)
+__device__ __forceinline__ void mbar_init(uint32_t a, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TB_WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
+
+// Orientation of round s of the circle method: for CTA `rank`, the visiting
+// block X (loaded into registers) and the home block Y, packed X | Y << 8.
+__device__ void cluster_schedule(int rank, uint16_t* out) {
+  for (int s = 0; s < CNB - 1; ++s) {
+    int ea[CL], eb[CL], owner[CL];
+    bool done[CL];
+    ea[0] = CNB - 1;
+    eb[0] = s;
+    for (int p = 1; p < CL; ++p) {
+      ea[p] = (s + p) % (CNB - 1);
+      eb[p] = (s - p + CNB - 1) % (CNB - 1);
+    }
+    for (int e = 0; e < CL; ++e) {
+      owner[e] = -1;
+      done[e] = false;
+    }
+    // every CTA homes two blocks, so the matching is a 2-regular multigraph on
+    // the CTAs: walk each cycle, giving every CTA the next unassigned edge
+    for (int u0 = 0; u0 < CL; ++u0) {
+      int u = u0;
+      while (!done[u]) {
+        int e = 0;
+        while (owner[e] >= 0 || ((ea[e] >> 1) != u && (eb[e] >> 1) != u)) ++e;
+        owner[e] = u;
+        done[u] = true;
+        const int y = ((ea[e] >> 1) == u) ? ea[e] : eb[e];
+        const int x = (y == ea[e]) ? eb[e] : ea[e];
+        if (u == rank) out[s] = (uint16_t)(x | (y << 8));
+        u = x >> 1;
+      }
+    }
+  }
+}
+
+struct JacobiC {
+  uint32_t base;  // local shared address of home column slot 0
+  double2* W;
+  int Mw, Nw, rank;
+  double tol2, offmax;
+
+  // block b holds columns [start(b), start(b) + ncl(b)), balanced to within one
+  __device__ int ncl(int b) const { return Nw / CNB + (b >= CNB - Nw % CNB ? 1 : 0); }
+  __device__ int start(int b) const { return b * (Nw / CNB) + max(0, b - (CNB - Nw % CNB)); }
+
+  __device__ uint32_t lcol(int b, int k) const { return base + (uint32_t)((b & 1) * CBC + k) * CCB; }
+  __device__ uint32_t lrow() const { return (threadIdx.x & 31) * 16u; }
+
+  // one pair: a in registers (A_REG) or local smem at sa; b in local smem at sb
+  template <bool A_REG>
+  __device__ __forceinline__ bool rot(HCol<8>& a, uint32_t sa, uint32_t sb, double& na, double& nb, double& da,
+                                      double& db) {
+    const uint32_t l = lrow();
+    double2 x[8], y[8];
+    double2 g = cz(), h = cz();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      x[q] = A_REG ? a.v[q] : lds2(sa + l + 512u * q);
+      y[q] = lds2(sb + l + 512u * q);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      cfmac(g, x[q], y[q]);
+      cfmac(h, x[q + 1], y[q + 1]);
+    }
+    double gr = g.x + h.x, gi = g.y + h.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      gr += __shfl_xor_sync(0xffffffffu, gr, o);
+      gi += __shfl_xor_sync(0xffffffffu, gi, o);
+    }
+    const double dd = da * db;
+    gr *= dd;
+    gi *= dd;
+    const Rot p = rot_params(gr, gi, na, nb, true, tol2);
+    if (!p.rot) return false;  // warp-uniform: every lane holds the same sums
+    {
+      double r;
+      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(na * nb));
+      offmax = fmax(offmax, p.g2 * r);
+    }
+    const double nan_ = na - p.tg, nbn = nb + p.tg;
+    const double inv = rcp_acc(dd);
+    const double r1 = p.tau * db * db * inv, r2 = p.tau * da * da * inv;
+    const double f1r = gr * r1, f1i = -gi * r1, f2r = gr * r2, f2i = gi * r2;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t o = l + 512u * q;
+      double2 nx, ny;
+      ny.x = fma(f2r, x[q].x, fma(-f2i, x[q].y, y[q].x));
+      ny.y = fma(f2r, x[q].y, fma(f2i, x[q].x, y[q].y));
+      nx.x = fma(-f1r, y[q].x, fma(f1i, y[q].y, x[q].x));
+      nx.y = fma(-f1r, y[q].y, fma(-f1i, y[q].x, x[q].y));
+      sts2(sb + o, ny);
+      if (A_REG) a.v[q] = nx;
+      else sts2(sa + o, nx);
+    }
+    da *= p.c;
+    db *= p.c;
+    const bool fa = nan_ < 0.5 * na, fb = nbn < 0.5 * nb;
+    na = nan_;
+    nb = nbn;
+    if (fa || fb) {  // cancellation: re-evaluate the transferred norm from the data
+      double ea = 0.0, eb = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        ea += abs2(A_REG ? a.v[q] : lds2(sa + l + 512u * q));
+        eb += abs2(lds2(sb + l + 512u * q));
+      }
+      ea = warp_sum(ea) * (da * da);
+      eb = warp_sum(eb) * (db * db);
+      if (fa) na = ea;
+      if (fb) nb = eb;
+    }
+    return true;
+  }
+
+  // TMA staging: every home column is one bulk copy of Mw x 16 B straight into
+  // its shared-memory slot (rows >= Mw and unused columns are zero-filled by
+  // the threads), all completing on one mbarrier
+  __device__ void load_home_tma(Smem& sm) {
+    const uint32_t mbar = sh_addr(&sm.cl_mbar);
+    if (threadIdx.x == 0) mbar_init(mbar, 1);
+    for (int s = 0; s < 2; ++s) {
+      const int b = 2 * rank + s, nc = ncl(b);
+      for (int e = threadIdx.x; e < CBC * 256; e += NT) {
+        const int k = e >> 8, y = e & 255;
+        if (k >= nc || y >= Mw) sts2(lcol(b, k) + 16u * y, cz());
+      }
+    }
+    // generic-proxy shared-memory traffic (earlier phases, the padding)
+    // before the async-proxy writes; W was written by the leader (generic)
+    asm volatile("fence.proxy.async.shared::cta;\n\tfence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    const int n0 = ncl(2 * rank), n1 = ncl(2 * rank + 1);
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) mbar_expect_tx(mbar, (uint32_t)((n0 + n1) * Mw * 16));
+      __syncwarp();
+      const int t = threadIdx.x, s = t >= n0 ? 1 : 0, k = t - s * n0;
+      if (t < n0 + n1) {
+        const int b = 2 * rank + s;
+        bulk_g2s(lcol(b, k), W + (size_t)(start(b) + k) * Mw, (uint32_t)(Mw * 16), mbar);
+      }
+    }
+    mbar_wait(mbar, 0);
+  }
+
+  __device__ void store_home_tma(Smem& sm) {
+    const int warp = threadIdx.x >> 5;
+    for (int t = warp; t < 2 * CBC; t += NWARP) {  // fold the scales in place
+      const int b = 2 * rank + t / CBC, k = t % CBC;
+      if (k >= ncl(b)) continue;
+      const double d = sm.dsc[start(b) + k];
+      if (d == 1.0) continue;
+      const uint32_t col = lcol(b, k) + lrow();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sts2(col + 512u * q, cscale(lds2(col + 512u * q), d));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const int n0 = ncl(2 * rank), n1 = ncl(2 * rank + 1);
+    if (threadIdx.x < 32) {
+      const int t = threadIdx.x, s = t >= n0 ? 1 : 0, k = t - s * n0;
+      if (t < n0 + n1) {
+        const int b = 2 * rank + s;
+        bulk_s2g(W + (size_t)(start(b) + k) * Mw, lcol(b, k), (uint32_t)(Mw * 16));
+      }
+      asm volatile("cp.async.bulk.commit_group;\n\tcp.async.bulk.wait_group 0;\n\tfence.proxy.async.global;" :::
+                       "memory");
+    }
+  }
+
+  __device__ void load_home() {
+    for (int s = 0; s < 2; ++s) {
+      const int b = 2 * rank + s, nc = ncl(b), c0 = start(b);
+      for (int e = threadIdx.x; e < CBC * 256; e += NT) {
+        const int k = e >> 8, y = e & 255;
+        const double2 v = (k < nc && y < Mw) ? W[(size_t)(c0 + k) * Mw + y] : cz();
+        sts2(lcol(b, k) + 16u * y, v);
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ void store_home(const Smem& sm) {
+    for (int s = 0; s < 2; ++s) {
+      const int b = 2 * rank + s, nc = ncl(b), c0 = start(b);
+      for (int e = threadIdx.x; e < nc * Mw; e += NT) {
+        const int k = e / Mw, y = e - k * Mw;
+        W[(size_t)(c0 + k) * Mw + y] = cscale(lds2(lcol(b, k) + 16u * y), sm.dsc[c0 + k]);
+      }
+    }
+  }
+
+  // fold the scales of the home columns into their data, refresh their
+  // norms, reduce |W|_F^2 over the cluster (fixed rank order) and zero the
+  // numerically dead columns
+  __device__ void fold_norms(Smem& sm, bool first) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < 2 * CBC; t += NWARP) {
+      const int b = 2 * rank + t / CBC, k = t % CBC;
+      if (k >= ncl(b)) continue;
+      const int c = start(b) + k;
+      const double d = first ? 1.0 : sm.dsc[c];
+      const uint32_t col = lcol(b, k) + lrow();
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double2 v = lds2(col + 512u * q);
+        if (d != 1.0) {
+          v = cscale(v, d);
+          sts2(col + 512u * q, v);
+        }
+        acc += abs2(v);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        sm.nrm[c] = acc;
+        sm.dsc[c] = 1.0;
+        sm.chg[c] = first ? 1 : ((sm.chg[c] >> 1) & 1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double part = 0.0;
+      for (int s = 0; s < 2; ++s)
+        for (int k = 0; k < ncl(2 * rank + s); ++k) part += sm.nrm[start(2 * rank + s) + k];
+      stcf(cl_map(sh_addr(&sm.cl_part[rank]), 0), part);
+      sm.flag = 0;
+      sm.offmax = 0.0;
+    }
+    cl_sync();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int r = 0; r < CL; ++r) t += ldcf(cl_map(sh_addr(&sm.cl_part[r]), 0));
+      sm.scale = t;
+    }
+    __syncthreads();
+    const double dead = 1e-28 * sm.scale;
+    for (int t = warp; t < 2 * CBC; t += NWARP) {
+      const int b = 2 * rank + t / CBC, k = t % CBC;
+      if (k >= ncl(b)) continue;
+      const int c = start(b) + k;
+      const double v = sm.nrm[c];
+      if (v < dead && v > 0.0) {
+        const uint32_t col = lcol(b, k) + lrow();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sts2(col + 512u * q, cz());
+        if (lane == 0) sm.nrm[c] = 0.0;
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ void within(Smem& sm) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = 2 * rank + (w >> 3), p = w & 7;
+    const int nb = ncl(b), nbp = nb + (nb & 1), c0 = start(b);
+    bool any = false;
+    for (int r = 0; r < CBC - 1; ++r) {
+      if (r < nbp - 1 && p < nbp / 2) {
+        int i, j;
+        rr_pair(r, p, nbp, i, j);
+        if (i < nb && j < nb && ((sm.chg[c0 + i] | sm.chg[c0 + j]) & 1)) {
+          double na = sm.nrm[c0 + i], nb2 = sm.nrm[c0 + j], da = sm.dsc[c0 + i], db = sm.dsc[c0 + j];
+          HCol<8> unused;
+          if (rot<false>(unused, lcol(b, i), lcol(b, j), na, nb2, da, db)) {
+            any = true;
+            if (lane == 0) {
+              sm.nrm[c0 + i] = na;
+              sm.nrm[c0 + j] = nb2;
+              sm.dsc[c0 + i] = da;
+              sm.dsc[c0 + j] = db;
+              sm.chg[c0 + i] |= 2;
+              sm.chg[c0 + j] |= 2;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (any && lane == 0) sm.flag = 1;
+  }
+
+  // visiting block X (home CTA X >> 1) against the local home block Y
+  __device__ void cross(int X, int Y, Smem& sm) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hx = X >> 1;
+    const int nP = ncl(X), nQ = ncl(Y), p0 = start(X), q0 = start(Y);
+    const bool vp = w < nP;
+    HCol<8> pc;
+    double np = 0.0, dp = 1.0;
+    uint32_t cp = 0;
+    const uint32_t pa = cl_map(lcol(X, w) + lrow(), hx);
+    if (vp) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pc.v[q] = ldc2(pa + 512u * q);
+      np = ldcf(cl_map(sh_addr(&sm.nrm[p0 + w]), hx));
+      dp = ldcf(cl_map(sh_addr(&sm.dsc[p0 + w]), hx));
+      cp = ldcb(cl_map(sh_addr(&sm.chg[p0 + w]), hx));
+    }
+    bool any = false;
+    for (int r = 0; r < CBC; ++r) {
+      const int c = (w + r) & (CBC - 1);
+      if (vp && c < nQ && ((cp | sm.chg[q0 + c]) & 1)) {
+        double nq = sm.nrm[q0 + c], dq = sm.dsc[q0 + c];
+        if (rot<true>(pc, 0u, lcol(Y, c), np, nq, dp, dq)) {
+          any = true;
+          cp |= 2;
+          if (lane == 0) {
+            sm.nrm[q0 + c] = nq;
+            sm.dsc[q0 + c] = dq;
+            sm.chg[q0 + c] |= 2;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (vp) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) stc2(pa + 512u * q, pc.v[q]);
+      if (lane == 0) {
+        stcf(cl_map(sh_addr(&sm.nrm[p0 + w]), hx), np);
+        stcf(cl_map(sh_addr(&sm.dsc[p0 + w]), hx), dp);
+        stcb(cl_map(sh_addr(&sm.chg[p0 + w]), hx), cp);
+      }
+    }
+    if (any && lane == 0) sm.flag = 1;
+  }
+
+  // cluster-wide "anything rotated" and largest relative off-diagonal of the
+  // sweep; true when the sweep converged
+  __device__ bool sweep_end(Smem& sm, int par) {
+    if ((threadIdx.x & 31) == 0 && offmax > 0.0) atomic_max_pos(&sm.offmax, offmax);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t fa = cl_map(sh_addr(&sm.cl_flag[par]), 0), oa = cl_map(sh_addr(&sm.cl_off[par]), 0);
+      asm volatile("atom.shared::cluster.or.b32 _, [%0], %1;" ::"r"(fa), "r"(sm.flag) : "memory");
+      asm volatile("atom.shared::cluster.max.u64 _, [%0], %1;" ::"r"(oa),
+                   "l"((unsigned long long)__double_as_longlong(sm.offmax))
+                   : "memory");
+    }
+    cl_sync();
+    if (threadIdx.x == 0) {
+      sm.cl_rflag = (int)ldcu(cl_map(sh_addr(&sm.cl_flag[par]), 0));
+      sm.cl_roff = ldcf(cl_map(sh_addr(&sm.cl_off[par]), 0));
+      if (rank == 0) {  // the other parity is next read after >= 1 more cluster barrier
+        sm.cl_flag[par ^ 1] = 0;
+        sm.cl_off[par ^ 1] = 0.0;
+      }
+    }
+    __syncthreads();
+    return sm.cl_rflag == 0 || sm.cl_roff < 1e-16 * TB_TOLSCALE;
+  }
+};
+
+// All CTAs of the cluster call this with the same arguments; returns Nw
+// (converged) or -Nw, with the rotated columns (scales folded) back in W.
+__device__ __noinline__ int jacobi_cluster(double2* W, int Mw, int Nw, int maxsweep, Smem& sm, double2* smem) {
+  JacobiC J;
+  J.W = W;
+  J.Mw = Mw;
+  J.Nw = Nw;
+  J.rank = cl_rank();
+  J.base = sh_addr(smem);
+  const double tol = fmax(sqrt((double)Mw), 4.0) * 4.440892098500626e-16 * TB_TOLSCALE;
+  J.tol2 = tol * tol;
+  if (threadIdx.x == 0) cluster_schedule(J.rank, sm.cl_sched);
+  if (sm.cl_tma) J.load_home_tma(sm);
+  else J.load_home();
+  int sweep = 0;
+  bool conv = false;
+  for (; sweep < maxsweep; ++sweep) {
+    J.fold_norms(sm, sweep == 0);
+    J.offmax = 0.0;
+    J.within(sm);
+    cl_sync();
+    for (int s = 0; s < CNB - 1; ++s) {
+      const int xy = sm.cl_sched[s];
+      J.cross(xy & 0xff, xy >> 8, sm);
+      cl_sync();
+    }
+    if (J.sweep_end(sm, sweep & 1)) {
+      conv = true;
+      break;
+    }
+  }
+  if (threadIdx.x == 0) sm.sweeps = sweep + 1;
+  if (sm.cl_tma) J.store_home_tma(sm);
+  else J.store_home(sm);
+  __threadfence();
+  cl_sync();
+  return conv ? Nw : -Nw;
+}
+
+// leader side: post the command, then take part as rank 0
+__device__ int jacobi_cluster_lead(double2* W, int Mw, int Nw, Smem& sm, double2* smem) {
+  if (threadIdx.x == 0) {
+    sm.cl_op = 1;
+    sm.cl_W = W;
+    sm.cl_Mw = Mw;
+    sm.cl_Nw = Nw;
+    sm.cl_maxsweep = sm.maxsweep;
+    sm.cl_flag[0] = sm.cl_flag[1] = 0;
+    sm.cl_off[0] = sm.cl_off[1] = 0.0;
+  }
+  __threadfence();  // W (global) as this CTA wrote it, before the followers load their blocks
+  __syncthreads();
+  cl_sync();
+  return jacobi_cluster(W, Mw, Nw, sm.maxsweep, sm, smem);
+}
+
+// ranks 1..7: serve the leader's cluster Jacobi calls until it posts op 0
+__device__ void cluster_follow(Smem& sm, double2* smem) {
+  for (;;) {
+    cl_sync();
+    if (threadIdx.x == 0) {
+      sm.cl_op = (int)ldcu(cl_map(sh_addr(&sm.cl_op), 0));
+      sm.cl_W = (double2*)ldcl(cl_map(sh_addr(&sm.cl_W), 0));
+      sm.cl_Mw = (int)ldcu(cl_map(sh_addr(&sm.cl_Mw), 0));
+      sm.cl_Nw = (int)ldcu(cl_map(sh_addr(&sm.cl_Nw), 0));
+      sm.cl_maxsweep = (int)ldcu(cl_map(sh_addr(&sm.cl_maxsweep), 0));
+      sm.cl_tma = (int)ldcu(cl_map(sh_addr(&sm.cl_tma), 0));
+    }
+    __syncthreads();
+    if (sm.cl_op == 0) {
+      cl_sync();  // the leader's shared memory stays alive until every follower read op 0
+      return;
+    }
+    jacobi_cluster(sm.cl_W, sm.cl_Mw, sm.cl_Nw, sm.cl_maxsweep, sm, smem);
+  }
+}
+
+// leader side: release the followers (end of the kernel)
+__device__ void cluster_release(Smem& sm) {
+  if (threadIdx.x == 0) sm.cl_op = 0;
+  __syncthreads();
+  cl_sync();
+  cl_sync();
+}
+
 // dispatcher: returns the number of (possibly padded) result columns in W;
 // sets status bit 0 on non-convergence
 __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* status) {
@@ -1507,7 +2072,8 @@ __device__ int jacobi(double2* W, int Mw, int Nw, Smem& sm, double2* smem, int* 
   else if (Mw <= 32 && Nw <= 128) neff = jacobi_half<2>(W, Mw, Nw, sm, smem);
   else if (Mw <= 64 && Nw <= 128) neff = jacobi_half<4>(W, Mw, Nw, sm, smem);
   else if (Mw <= 128 && Nw <= 128) neff = jacobi_half<8>(W, Mw, Nw, sm, smem);
-  else if (Mw <= 256 && Nw <= 256) neff = jacobi_wide(W, Mw, Nw, sm, smem);
+  else if (Mw <= 256 && Nw <= 256)
+    neff = sm.cluster > 1 ? jacobi_cluster_lead(W, Mw, Nw, sm, smem) : jacobi_wide(W, Mw, Nw, sm, smem);
   else {
     const int sw = hestenes(W, Mw, Nw, sm);
     neff = (sw > MAXSWEEP) ? -Nw : Nw;
@@ -2706,12 +3272,25 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
   Ctx cx;
   cx.job = &job;
   cx.cap = cap;
-  cx.mps = job.ws_mps + job.mps_stride * blockIdx.x;
-  cx.W = job.ws_W + job.mat_stride * blockIdx.x;
-  cx.W0 = job.ws_W0 + job.mat_stride * blockIdx.x;
-  cx.X = job.ws_X + job.mat_stride * blockIdx.x;
+  // cluster launch: rank 0 of each cluster runs circuits, ranks 1..7 only
+  // serve its wide Jacobi calls (cluster_follow)
+  const int wid = job.cluster > 1 ? blockIdx.x / job.cluster : blockIdx.x;
+  if (job.cluster > 1) {
+    if (threadIdx.x == 0) sm.cluster = job.cluster;
+    cl_sync();  // every CTA of the cluster is running before any DSMEM access
+    if (cl_rank() != 0) {
+      cluster_follow(sm, dyn_smem);
+      return;
+    }
+  }
+  cx.mps = job.ws_mps + job.mps_stride * wid;
+  cx.W = job.ws_W + job.mat_stride * wid;
+  cx.W0 = job.ws_W0 + job.mat_stride * wid;
+  cx.X = job.ws_X + job.mat_stride * wid;
   cx.tile = dyn_smem;
   if (threadIdx.x == 0) {
+    sm.cluster = job.cluster;
+    sm.cl_tma = job.cluster_tma;
     sm.flops = 0.0;
     sm.prof = job.prof;
     sm.tmem_on = job.qrcp_tmem;
@@ -2872,6 +3451,7 @@ __global__ void __launch_bounds__(NT, 1) ensemble_kernel(const __grid_constant__
   }
   if (threadIdx.x == 0) job.flops[blockIdx.x] += sm.flops;
   if (job.qrcp_tmem) tmem_free(sm);
+  if (job.cluster > 1) cluster_release(sm);
 }
 
 // ----------------------------------------------------------------------------
@@ -2965,9 +3545,19 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
                                                     int kcut) {
   extern __shared__ double2 dyn_smem[];
   __shared__ Smem sm;
-  const int b = blockIdx.x;
+  const bool clu = (precond >> 2) & 1;  // 8-CTA clusters: one matrix per cluster
+  const int b = clu ? blockIdx.x / CL : blockIdx.x;
   const int K = min(m, n);
+  if (clu) {
+    cl_sync();
+    if (cl_rank() != 0) {
+      cluster_follow(sm, dyn_smem);
+      return;
+    }
+  }
   if (threadIdx.x == 0) {
+    sm.cluster = clu ? CL : 0;
+    sm.cl_tma = (precond >> 3) & 1;
     sm.prof = prof;
     sm.kcut = (kcut > 0 && kcut < K) ? kcut : MAXDIM;
     sm.tmem_on = (precond >> 1) & 1;
@@ -3017,6 +3607,7 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
         [&](int y, int x) { return W0[(size_t)x * m + y]; },
         [&](int c, int x, double2 v) { vh[(size_t)b * K * n + (size_t)c * n + x] = v; }, dyn_smem);
   if (precond & 2) tmem_free(sm);
+  if (clu) cluster_release(sm);
 }
 
 constexpr size_t kTileBytes = 2 * TK * TLD * sizeof(double2);
@@ -3179,6 +3770,8 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
     if (job.max_sweeps < 1 || job.max_sweeps > tb::MAXSWEEP) job.max_sweeps = tb::MAXSWEEP;
     const char* fi = getenv("TB_FAULT_INJECT");
     job.inject = fi ? atoi(fi) : 0;
+    const char* ct = getenv("TB_CLUSTER_TMA");
+    job.cluster_tma = ct ? atoi(ct) : 1;
   }
   job.floor = d->svalue_floor;
   job.n_samples = d->n_samples;
@@ -3231,7 +3824,24 @@ int launch(tb_ctx* c, tb::Job& job, int grid, cudaStream_t st, double* o_flops, 
   TB_CUDA(c, cudaMemsetAsync(c->dflops, 0, grid * sizeof(double), st));
   TB_CUDA(c, cudaMemsetAsync(c->dprof, 0, 64 * sizeof(unsigned long long), st));
   if (kernel_ms) TB_CUDA(c, cudaEventRecord(c->e0, st));
-  tb::ensemble_kernel<<<grid, tb::NT, smem, st>>>(job);
+  if (job.cluster > 1) {
+    TB_CUDA(c, cudaFuncSetAttribute(tb::ensemble_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)job.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(tb::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TB_CUDA(c, cudaLaunchKernelEx(&cfg, tb::ensemble_kernel, job));
+  } else {
+    tb::ensemble_kernel<<<grid, tb::NT, smem, st>>>(job);
+  }
   TB_CUDA(c, cudaGetLastError());
   if (kernel_ms) TB_CUDA(c, cudaEventRecord(c->e1, st));
   if (o_flops) {
@@ -3271,6 +3881,39 @@ int read_status(tb_ctx* c, bool nonconv_ok = false) {
   int st = 0;
   const int rc = take_status(c, &st);
   return rc ? rc : status_rc(c, st, nonconv_ok);
+}
+
+// Wide Jacobi in 8-CTA clusters (jacobi_cluster): used when the bond
+// capacity admits 256-row problems (cap > 64).  tb_run_stream (one circuit)
+// uses it unless TB_CLUSTER=0; the ensemble calls only with
+// TB_CLUSTER_ENSEMBLE=1 (one circuit per cluster instead of per SM).
+int cluster_mode(int cap, bool ensemble) {
+  if (cap <= 64) return 0;
+  const char* e = getenv(ensemble ? "TB_CLUSTER_ENSEMBLE" : "TB_CLUSTER");
+  if (ensemble) return (e && atoi(e)) ? tb::CL : 0;
+  return (e && !atoi(e)) ? 0 : tb::CL;
+}
+
+// co-resident 8-CTA clusters of ensemble_kernel on this device
+int max_clusters(tb_ctx* c, int* out) {
+  const size_t smem = tb::kDynSmem;
+  TB_CUDA(c, cudaFuncSetAttribute(tb::ensemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = tb::CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(tb::CL * 32);
+  cfg.blockDim = dim3(tb::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  TB_CUDA(c, cudaOccupancyMaxActiveClusters(&n, tb::ensemble_kernel, &cfg));
+  if (n < 1) return fail(c, TB_ECUDA, "no 8-CTA cluster of the engine kernel fits on this device");
+  *out = n;
+  return TB_OK;
 }
 
 // device copies of a host descriptor/outputs; frees on destruction
@@ -3494,7 +4137,8 @@ int tb_run_stream(tb_ctx* c, double* buf, int64_t n, int64_t cap, int64_t* dims,
   memset(&o, 0, sizeof(o));
   tb::Job job = make_job(c, &d, &o);
   job.slot_mode = 1;  // continue the uploaded state (no reset)
-  rc = launch(c, job, 1, 0, nullptr, nullptr);
+  job.cluster = cluster_mode((int)cap, false);
+  rc = launch(c, job, job.cluster > 1 ? job.cluster : 1, 0, nullptr, nullptr);
   if (rc) return rc;
   TB_CUDA(c, cudaDeviceSynchronize());
   TB_CUDA(c, cudaMemcpy(buf, c->mps, site_bytes, cudaMemcpyDeviceToHost));
@@ -3601,9 +4245,29 @@ int tb_svd_trunc(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n
   TB_CUDA(c, cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const char* pe = getenv("TB_PRECOND");
   const char* tm = getenv("TB_QRCP_TMEM");
-  const int precond = (pe ? atoi(pe) : 1) | ((!tm || atoi(tm)) ? 2 : 0);
-  tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->X, c->mat_stride, ds, du, dvh,
-                                               c->dscratch + 1, c->dprof, precond, (int)kcut);
+  const char* ce = getenv("TB_CLUSTER");
+  const bool clu = ce && atoi(ce) && (m > 128 || n > 128);  // unit-test surface of jacobi_cluster
+  const char* ct = getenv("TB_CLUSTER_TMA");
+  const int precond = (pe ? atoi(pe) : 1) | ((!tm || atoi(tm)) ? 2 : 0) | (clu ? 4 : 0) | ((!ct || atoi(ct)) ? 8 : 0);
+  if (clu) {
+    TB_CUDA(c, cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = tb::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(batch * tb::CL));
+    cfg.blockDim = dim3(tb::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TB_CUDA(c, cudaLaunchKernelEx(&cfg, tb::svd_kernel, (const double2*)da, (int)m, (int)n, c->W, c->W0, c->X,
+                                  c->mat_stride, ds, du, dvh, c->dscratch + 1, c->dprof, precond, (int)kcut));
+  } else {
+    tb::svd_kernel<<<(int)batch, tb::NT, smem>>>(da, (int)m, (int)n, c->W, c->W0, c->X, c->mat_stride, ds, du, dvh,
+                                                 c->dscratch + 1, c->dprof, precond, (int)kcut);
+  }
   TB_CUDA(c, cudaGetLastError());
   TB_CUDA(c, cudaDeviceSynchronize());
   TB_CUDA(c, cudaMemcpy(s, ds, batch * k * sizeof(double), cudaMemcpyDeviceToHost));
@@ -3617,14 +4281,18 @@ int tb_run_ensemble_device(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out
   int rc = validate_desc(c, d, o);
   if (rc) return rc;
   if (d->n_samples == 0) return TB_OK;
-  const int grid = d->n_samples < c->sms ? d->n_samples : c->sms;
+  const int cl = cluster_mode(d->cap, true);
+  int units = c->sms;  // persistent CTAs, or clusters
+  if (cl > 1 && (rc = max_clusters(c, &units))) return rc;
+  const int grid = d->n_samples < units ? d->n_samples : units;
   rc = ensure_workspace(c, grid, d->n, d->cap);
   if (rc) return rc;
   c->state_n = c->state_cap = -1;  // whole-sample runs reuse the slot memory
   ++c->gen;
   tb::Job job = make_job(c, d, o);
   job.slot_mode = 0;
-  return launch(c, job, grid, (cudaStream_t)stream, o->flops, o->kernel_ms);
+  job.cluster = cl;
+  return launch(c, job, cl > 1 ? grid * cl : grid, (cudaStream_t)stream, o->flops, o->kernel_ms);
 }
 
 int tb_run_ensemble(tb_ctx* c, const tb_ensemble_desc* d, tb_ensemble_out* o) {
@@ -3667,8 +4335,11 @@ int tb_step_device(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, void* 
   job.reset = sd->reset;
   job.sum_row = sd->sum_row;
   job.order = sd->order;
-  const int grid = d->n_samples < c->sms ? d->n_samples : c->sms;
-  return launch(c, job, grid, (cudaStream_t)stream, o->flops, o->kernel_ms);
+  job.cluster = cluster_mode(d->cap, true);
+  int units = c->sms;
+  if (job.cluster > 1 && (rc = max_clusters(c, &units))) return rc;
+  const int grid = d->n_samples < units ? d->n_samples : units;
+  return launch(c, job, job.cluster > 1 ? grid * job.cluster : grid, (cudaStream_t)stream, o->flops, o->kernel_ms);
 }
 
 int tb_step(tb_ctx* c, const tb_step_desc* sd, tb_ensemble_out* o, int64_t sum_rows) {

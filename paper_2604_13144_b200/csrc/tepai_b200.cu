@@ -2028,7 +2028,12 @@ __device__ int jacobi_cluster_lead(double2* W, int Mw, int Nw, Smem& sm, double2
     sm.cl_flag[0] = sm.cl_flag[1] = 0;
     sm.cl_off[0] = sm.cl_off[1] = 0.0;
   }
-  __threadfence();  // W (global) as this CTA wrote it, before the followers load their blocks
+  // W (global) as this CTA wrote it, before the followers load their blocks.
+  // The followers read it through the async proxy (TMA bulk loads): the
+  // WRITER orders its generic-proxy stores before them (without this fence a
+  // follower's bulk load could return the buffer's previous contents)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence();
   __syncthreads();
   cl_sync();
   return jacobi_cluster(W, Mw, Nw, sm.maxsweep, sm, smem);

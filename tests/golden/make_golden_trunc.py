@@ -43,7 +43,7 @@ sys.path.insert(0, REF)
 import numpy as np  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CACHE = "/tmp/golden_trunc"
+CACHE = os.environ.get("GOLDEN_TRUNC_CACHE", "/tmp/golden_trunc")
 DELTA = math.pi / 2**7
 CONFIGS = {
     # name: (n, ham_seed, circ_seed, n_steps, T, chi, n_samples)

@@ -54,6 +54,11 @@ void tb_destroy(tb_ctx* ctx);
 const char* tb_last_error(const tb_ctx* ctx);
 /* Number of SMs of the bound device (persistent-grid size). */
 int tb_num_sms(const tb_ctx* ctx);
+/* Persistent CTAs that run circuits of bond capacity `cap` concurrently:
+ * tb_num_sms() for cap > 32; twice that for cap <= 32, where the
+ * small-problem engine keeps two circuits resident per SM (TB_SMALL_ENGINE=0
+ * disables it).  Size slot pools as a multiple of this. */
+int tb_num_ctas(const tb_ctx* ctx, int64_t cap);
 /* Read and clear the context's sticky device status word (device-buffer
  * calls do not synchronize, so they report through it): bit 0 = a Jacobi SVD
  * did not converge, bit 2 = a slot was continued (reset = 0) although its
@@ -172,7 +177,7 @@ int tb_run_ensemble_device(tb_ctx* ctx, const tb_ensemble_desc* desc, tb_ensembl
  * segment (base.gates / gate_offsets indexed by slot), optionally restarting
  * it from the product state first (reset[slot] = 1), measures <Z_j> at the
  * segment's checkpoints and adds the signed fixed-point values to estimator
- * row sum_row[slot][c].  The persistent CTAs (min(n_slots, tb_num_sms()))
+ * row sum_row[slot][c].  The persistent CTAs (min(n_slots, tb_num_ctas()))
  * take slots from an atomic queue, in the order given by `order` (a
  * permutation of the slots, e.g. by decreasing predicted cost; NULL = slot
  * order), so more slots than SMs balance the per-segment work.  The first

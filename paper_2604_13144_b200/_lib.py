@@ -14,7 +14,7 @@ LIB_NAME = "libtepai_b200.so"
 LIB_PATH = os.environ.get("TB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 EXPORTED = (
-    "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_take_status", "tb_debug_profile",
+    "tb_version", "tb_create", "tb_destroy", "tb_last_error", "tb_num_sms", "tb_num_ctas", "tb_take_status", "tb_debug_profile",
     "tb_run_stream",
     "tb_expectation", "tb_expectation_batch", "tb_svd", "tb_svd_trunc", "tb_run_ensemble", "tb_run_ensemble_device", "tb_step", "tb_step_device",
 )
@@ -73,6 +73,7 @@ def load() -> ctypes.CDLL:
         lib.tb_last_error.argtypes = [vp]
         lib.tb_last_error.restype = ctypes.c_char_p
         lib.tb_num_sms.argtypes = [vp]
+        lib.tb_num_ctas.argtypes = [vp, i64]
         lib.tb_debug_profile.argtypes = [vp, vp]
         lib.tb_take_status.argtypes = [vp, vp]
         lib.tb_run_stream.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp, vp, vp, i64, i64, dbl, vp, vp]

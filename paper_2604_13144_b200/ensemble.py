@@ -375,7 +375,7 @@ class SlotPipeline:
         if step_engine is None:
             self._own = _lib.PrivateContext(device)
             self.ctx = self._own.ctx
-            sms = _lib.load().tb_num_sms(self.ctx)
+            sms = _lib.load().tb_num_ctas(self.ctx, int(self.proto.cap))  # persistent CTAs for this bond capacity
         else:
             if not n_slots:
                 raise ValueError("an injected step engine needs an explicit n_slots")

@@ -91,8 +91,8 @@ def test_chi128_truncated_ring_cluster_vs_single_cta(engine, monkeypatch):
 def test_cluster_ensemble_matches_per_sm_ensemble(engine, monkeypatch):
     n = 16
     ham = tb.build_spin_ring(n, 1.0, 3)
-    cfg = tb.PaiConfig(math.pi / 2**6, 40, 1.0)
-    ck = [10, 20, 30, 40]
+    cfg = tb.PaiConfig(math.pi / 2**6, 50, 1.0)
+    ck = [10, 20, 30, 40, 50]
     runs = {}
     for cl in ("0", "1"):
         monkeypatch.setenv("TB_CLUSTER_ENSEMBLE", cl)

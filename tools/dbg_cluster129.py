@@ -1,4 +1,4 @@
-"""Debug: where does the cluster SVD of the graded 129x129 matrix lose orthogonality?"""
+"""Debug: which switch removes the cluster-Jacobi failures?"""
 import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -13,7 +13,7 @@ def svd_gpu(a):
     engine.check(lib.tb_svd(ctx, a.ctypes.data, b, m, n, s.ctypes.data, u.ctypes.data, vh.ctypes.data), ctx)
     return u, s, vh
 
-def mat(m, n):
+def mats(m, n):
     rng = np.random.default_rng(m * 1000 + n)
     k = min(m, n)
     q1, _ = np.linalg.qr(rng.normal(size=(m, k)) + 1j * rng.normal(size=(m, k)))
@@ -21,23 +21,29 @@ def mat(m, n):
     sv = np.logspace(0, -14, k)
     if k >= 8:
         sv[-(k // 8):] = 0.0
-    return np.stack([(q1 * sv) @ q2.conj().T])
+    return np.stack([(q1 * sv) @ q2.conj().T, rng.normal(size=(m, n)) + 1j * rng.normal(size=(m, n))])
 
-for shape in [(129, 129), (129, 129), (136, 256), (256, 256)]:
-    a = mat(*shape)
-    for env in [dict(TB_CLUSTER="1", TB_PRECOND="1", TB_CLUSTER_TMA="1"), dict(TB_CLUSTER="1", TB_PRECOND="1", TB_CLUSTER_TMA="0"),
-                dict(TB_CLUSTER="0", TB_PRECOND="1"), dict(TB_CLUSTER="1", TB_PRECOND="0", TB_CLUSTER_TMA="1")]:
-        for k in ("TB_CLUSTER", "TB_PRECOND", "TB_CLUSTER_TMA"):
-            os.environ.pop(k, None)
-        os.environ.update(env)
-        for rep in range(12):
-            u, s, vh = svd_gpu(a)
-            live = s[0] > 1e-10 * s[0][0]
-            uu = u[0][:, live]
-            g = np.abs(uu.conj().T @ uu - np.eye(uu.shape[1]))
-            i, j = np.unravel_index(np.argmax(g), g.shape)
-            big = np.argwhere(g > 1e-12)
-            if rep < 1 or g.max() > 1e-12:
-              print(shape, env, "rep", rep, "max", g.max(), "at", (i, j), "sig", s[0][i] / s[0][0], s[0][j] / s[0][0],
-                  "n>1e-12:", len(big), "first:", big[:6].tolist(), flush=True)
-        print(shape, env, "done 12 reps", flush=True)
+def errs(a, u, s, vh):
+    out = []
+    for b in range(a.shape[0]):
+        ref = np.linalg.svd(a[b], compute_uv=False)
+        e_s = np.max(np.abs(s[b] - ref)) / ref[0]
+        e_r = np.linalg.norm((u[b] * s[b]) @ vh[b] - a[b]) / np.linalg.norm(a[b])
+        live = s[b] > 1e-10 * s[b][0]
+        uu = u[b][:, live]
+        e_o = np.abs(uu.conj().T @ uu - np.eye(uu.shape[1])).max()
+        out.append((e_s, e_r, e_o))
+    return out
+
+for shape in [(256, 17), (160, 250), (129, 129), (256, 256), (136, 256)]:
+    a = mats(*shape)
+    for pre in ("0", "1"):
+        for dbg in ("0", "1", "2", "3"):
+            os.environ.update(TB_CLUSTER="1", TB_PRECOND=pre, TB_CLUSTER_TMA="1", TB_CL_DBG=dbg)
+            worst = np.zeros(3); bad = 0
+            for rep in range(6):
+                e = np.array(errs(a, *svd_gpu(a)))
+                worst = np.maximum(worst, e.max(axis=0))
+                bad += int(e[:, 0].max() > 1e-13 or e[:, 1].max() > 1e-12 or e[:, 2].max() > 1e-12)
+            print(shape, "precond", pre, "dbg", dbg, "(1: no offmax shortcut, 2: no pair skipping)", "bad reps", bad, "/ 6",
+                  "worst sv %.1e rec %.1e orth %.1e" % tuple(worst), flush=True)

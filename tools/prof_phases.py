@@ -1,6 +1,8 @@
 """Cycle breakdown of the batched 128x128 SVD kernel (diagnostic counters)."""
-import os, sys; sys.path.insert(0, "."); import __graft_entry__; __graft_entry__.build(profile=True)  # noqa: E702
+import os, sys; sys.path.insert(0, "."); import __graft_entry__  # noqa: E702
+# the library path is bound when the package is first imported (inside build()): set it before
 os.environ.setdefault("TB_PROFILE", "1"); os.environ.setdefault("TB_LIB", __graft_entry__.LIB_PROF)  # phase counters: diagnostics build
+__graft_entry__.build(profile=True)
 import sys, numpy as np
 sys.path.insert(0, ".")
 from paper_2604_13144_b200 import _lib

@@ -1,7 +1,9 @@
 """Batched 128x128 complex SVD through tb_svd (one CTA per matrix) — the
 Jacobi kernel in isolation, for timing and ncu.  usage: prof_svd.py [batch] [reps] [m] [n]"""
-import os, sys; sys.path.insert(0, "."); import __graft_entry__; __graft_entry__.build(profile=True)  # noqa: E702
+import os, sys; sys.path.insert(0, "."); import __graft_entry__  # noqa: E702
+# the library path is bound when the package is first imported (inside build()): set it before
 os.environ.setdefault("TB_PROFILE", "1"); os.environ.setdefault("TB_LIB", __graft_entry__.LIB_PROF)  # phase counters: diagnostics build
+__graft_entry__.build(profile=True)
 import sys, time
 import numpy as np
 sys.path.insert(0, ".")

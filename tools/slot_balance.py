@@ -1,8 +1,10 @@
 """Load balance of the slot-mode step (bench definition): per launch, kernel
 time vs the mean per-CTA busy time (clock64 counter prof[7] / CTAs / clock).
 usage: python tools/slot_balance.py [steps] [slots]"""
-import os, sys; sys.path.insert(0, "."); import __graft_entry__; __graft_entry__.build(profile=True)  # noqa: E702
+import os, sys; sys.path.insert(0, "."); import __graft_entry__  # noqa: E702
+# the library path is bound when the package is first imported (inside build()): set it before
 os.environ.setdefault("TB_PROFILE", "1"); os.environ.setdefault("TB_LIB", __graft_entry__.LIB_PROF)  # phase counters: diagnostics build
+__graft_entry__.build(profile=True)
 import math, sys
 import numpy as np
 sys.path.insert(0, ".")

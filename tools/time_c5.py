@@ -6,8 +6,10 @@ The circuits are the C5 TE-PAI stage cut to MAX_STEP Trotter steps at the same
 step size (PaiConfig(delta, MAX_STEP, MAX_STEP / 100)): identical per-step
 angles and gate statistics, so the rate extrapolates linearly to 100 steps.
 usage: python tools/time_c5.py N_SAMPLES MAX_STEP [N_SITES]"""
-import os, sys; sys.path.insert(0, "."); import __graft_entry__; __graft_entry__.build(profile=True)  # noqa: E702
+import os, sys; sys.path.insert(0, "."); import __graft_entry__  # noqa: E702
+# the library path is bound when the package is first imported (inside build()): set it before
 os.environ.setdefault("TB_PROFILE", "1"); os.environ.setdefault("TB_LIB", __graft_entry__.LIB_PROF)  # phase counters: diagnostics build
+__graft_entry__.build(profile=True)
 import math, sys, time
 import numpy as np
 sys.path.insert(0, ".")

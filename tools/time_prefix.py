@@ -1,7 +1,9 @@
 """Time the engine on a prefix of a config's circuits (exploration tool).
 usage: python tools/time_prefix.py N_SITES CHI HAM_SEED CIRC_SEED STEPS T N_SAMPLES MAX_STEP"""
-import os, sys; sys.path.insert(0, "."); import __graft_entry__; __graft_entry__.build(profile=True)  # noqa: E702
+import os, sys; sys.path.insert(0, "."); import __graft_entry__  # noqa: E702
+# the library path is bound when the package is first imported (inside build()): set it before
 os.environ.setdefault("TB_PROFILE", "1"); os.environ.setdefault("TB_LIB", __graft_entry__.LIB_PROF)  # phase counters: diagnostics build
+__graft_entry__.build(profile=True)
 import math, sys, time
 import numpy as np
 sys.path.insert(0, ".")
@@ -40,3 +42,4 @@ print("jacobi overheads (share of total): build_l %.3f staging %.3f refresh %.3f
 print("qrcp sub-phases (cycles/step, thread 0 view): pivot %.0f publish %.0f normalise %.0f update %.0f barrier %.0f" % tuple(
     pr[32:37] / max(pr[15], 1)))
 print("two-site front end (share of total): theta GEMM %.3f gate pass %.3f" % (pr[30] / tot, pr[31] / tot))
+print("gram screen: calls %d, k cycles per call %.0f, share of total %.3f" % (pr[39], pr[38] / max(pr[39], 1) / 1e3, pr[38] / tot))

@@ -98,7 +98,10 @@ struct Job {
 // small-problem engine (bond capacity <= 32, two CTAs per SM)
 #define TB_ENGINE_NS tbs
 #define TB_ENGINE_MAXCAP 32
-#define TB_ENGINE_MINB 2
+#ifndef TB_SMALL_MINB
+#define TB_SMALL_MINB 2
+#endif
+#define TB_ENGINE_MINB TB_SMALL_MINB
 #define TB_ENGINE_SMALL 1
 #include "tepai_engine.cuh"
 #undef TB_ENGINE_NS
@@ -309,7 +312,11 @@ bool small_engine(int cap) {
 }
 
 // persistent CTAs that run circuits of bond capacity `cap` concurrently
-int persistent_ctas(const tb_ctx* c, int cap) { return small_engine(cap) ? 2 * c->sms : c->sms; }
+int persistent_ctas(const tb_ctx* c, int cap) {
+  if (!small_engine(cap)) return c->sms;
+  const char* e = getenv("TB_SMALL_CTAS_PER_SM");  // debug: 1 = one resident CTA per SM
+  return (e && atoi(e) == 1) ? c->sms : 2 * c->sms;
+}
 
 // launch the persistent kernel (+ FLOP reduction into o_flops) on stream st
 int launch(tb_ctx* c, tb::Job& job, int grid, cudaStream_t st, double* o_flops, float* kernel_ms) {

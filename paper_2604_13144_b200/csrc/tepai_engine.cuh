@@ -72,11 +72,11 @@ struct Smem {
   double sig[MAXDIM];
   double nrm[MAXDIM];
   double dsc[MAXDIM];        // Jacobi column scales (true column = dsc * stored)
-  double wbest[32];          // per-half-warp pivot candidates (QRCP)
+  double wbest[2][32];       // per-half-warp pivot candidates (QRCP), double-buffered by step parity in qrcp_mgs
   int qcnt[3 * 32];          // cross-phase Q visit counters (per slot, column)
   unsigned char chg[MAXDIM]; // bit0: rotated in the previous sweep, bit1: in this sweep, bit2: tail column
   int jncol[4];              // live columns per Jacobi block slot
-  int wbidx[32];
+  int wbidx[2][32];
   double nref[MAXDIM];       // QRCP reference norms; after the Jacobi: 1 / sigma of the kept columns
   int qperm[MAXDIM];
   int qpinv[MAXDIM];
@@ -2245,7 +2245,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     if (threadIdx.x == 0) sm.scale = 1e-28 * t;  // dead threshold on residual norm^2
   }
   // per-half pivot candidate over the owned columns (lanes 0-3 of the half)
-  auto local_best = [&]() {
+  auto local_best = [&](int buf) {
     const int c = (hl < 3) ? hw + 32 * hl : cg;
     const bool ok = hl < 4 && c < Mw && (hl == 3 || c < nsm);
     double best = ok ? sm.nrm[c] : -1.0;
@@ -2257,11 +2257,11 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
       if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
     }
     if (hl == 0) {
-      sm.wbest[hw] = best;
-      sm.wbidx[hw] = bi;
+      sm.wbest[buf][hw] = best;
+      sm.wbidx[buf][hw] = bi;
     }
   };
-  local_best();
+  local_best(0);
   __syncthreads();
   const double dead = sm.scale;
   const int rmax = min(Mw, Nw);
@@ -2273,8 +2273,15 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     // (non-negative) norm with its 7 low bits replaced by 127 - column, so one
     // redux.max picks the largest norm (to ~1e-6 relative; near-ties go to the
     // lowest index, which is immaterial for the preconditioner)
-    const int wi = sm.wbidx[lane];
-    const double wv = sm.wbest[lane];
+    // The candidates of step j live in buffer j & 1 and those of step j + 1 go
+    // to the other one: a step has a single barrier (at its end), so a half
+    // that finishes its updates early writes its next candidate while a slower
+    // warp may not have read this step's yet.  With one buffer that warp could
+    // pick a different pivot than the rest of the CTA (seen on the GPU with
+    // two resident CTAs per SM: run-to-run differences at rounding level and
+    // sporadic faults on 32x32 problems).
+    const int wi = sm.wbidx[j & 1][lane];
+    const double wv = sm.wbest[j & 1][lane];
     const unsigned key = (wi >= 0 && wv > dead) ? ((unsigned)__double2hiint(wv) & 0xFFFFFF80u) | (unsigned)(127 - wi) : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
     if (kmax == 0u) break;
@@ -2366,7 +2373,7 @@ __device__ int qrcp_mgs(const double2* Y, int Nw, int Mw, double2* R, Smem& sm, 
     }
     if (hw == owner && hl == 0) sm.nrm[p] = -1.0;
     __syncwarp();
-    local_best();
+    local_best((j + 1) & 1);
     const long long tt4 = prof_fine();
     __syncthreads();
     tqd += tt4 - tt3;
@@ -2496,8 +2503,8 @@ __device__ __noinline__ int qrcp_tmem(const double2* Y, int Nw, int Mw, double2*
       if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
     }
     if (hl == 0) {
-      sm.wbest[hw] = best;
-      sm.wbidx[hw] = bi;
+      sm.wbest[0][hw] = best;
+      sm.wbidx[0][hw] = bi;
     }
   };
   local_best();
@@ -2506,8 +2513,8 @@ __device__ __noinline__ int qrcp_tmem(const double2* Y, int Nw, int Mw, double2*
   const int rmax = min(Mw, Nw);
   int j = 0;
   for (; j < rmax; ++j) {
-    const int wi = sm.wbidx[lane];
-    const double wv = sm.wbest[lane];
+    const int wi = sm.wbidx[0][lane];
+    const double wv = sm.wbest[0][lane];
     const unsigned key = (wi >= 0 && wv > dead) ? ((unsigned)__double2hiint(wv) & 0xFFFFFF80u) | (unsigned)(127 - wi) : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
     if (kmax == 0u) break;
@@ -2702,8 +2709,8 @@ __device__ int qrcp_wide(double2* Y, int Nw, int Mw, double2* R, Smem& sm, doubl
       if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
     }
     if (hl == 0) {
-      sm.wbest[hw] = best;
-      sm.wbidx[hw] = bi;
+      sm.wbest[0][hw] = best;
+      sm.wbidx[0][hw] = bi;
     }
   };
   local_best();
@@ -2713,8 +2720,8 @@ __device__ int qrcp_wide(double2* Y, int Nw, int Mw, double2* R, Smem& sm, doubl
   int j = 0;
   for (; j < rmax; ++j) {
     // global pivot: same packed-key redux as qrcp_mgs (8 index bits here)
-    const int wi = sm.wbidx[lane];
-    const double wv = sm.wbest[lane];
+    const int wi = sm.wbidx[0][lane];
+    const double wv = sm.wbest[0][lane];
     const unsigned key =
         (wi >= 0 && wv > dead) ? ((unsigned)__double2hiint(wv) & 0xFFFFFF00u) | (unsigned)(255 - wi) : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);

@@ -872,12 +872,13 @@ struct JacobiH {
   __device__ __forceinline__ bool blk_any(unsigned bm, int a, int b) const { return (bm >> (4 * a + b)) & 1u; }
   // column positions are those of the sweep's start: after the mid-sweep
   // exchange of slots 0 and 3 a position maps back to where the screen saw it
+  __device__ __forceinline__ int opos(int c) const {
+    return swapped ? (c < JB ? c + 3 * JB : (c >= 3 * JB ? c - 3 * JB : c)) : c;
+  }
   __device__ __forceinline__ bool flagged(const Smem& sm, int ci, int cj) const {
     if (!screen) return true;
-    if (swapped) {
-      ci = ci < JB ? ci + 3 * JB : (ci >= 3 * JB ? ci - 3 * JB : ci);
-      cj = cj < JB ? cj + 3 * JB : (cj >= 3 * JB ? cj - 3 * JB : cj);
-    }
+    ci = opos(ci);
+    cj = opos(cj);
     return (sm.pbits[ci][cj >> 5] >> (cj & 31)) & 1u;
   }
 
@@ -949,6 +950,10 @@ struct JacobiH {
   // (reductions, rotation parameters) then overlap other halves' FP64 work.
   __device__ void cross(HCol<HR>& pc, double& np, double& dp, int nP, int sp, int sq0, int sq1, int sq2, int S,
                         Smem& sm) {
+    if (screen && sm.screen_on > 1) {
+      cross_screened(pc, np, dp, sp, sq0, sq1, sq2, S, sm);
+      return;
+    }
     const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
     const bool vp = hw < nP;
     bool any = false;
@@ -992,6 +997,93 @@ struct JacobiH {
     }
     __syncthreads();
     if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
+    if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[14], (unsigned long long)(prof_clock() - tc0));
+  }
+
+  // Cross phase of a SCREENED sweep: only the flagged pairs are visited, and
+  // only they synchronise.  Half k still takes its Q columns in the order of
+  // cross() (visit m: column (k + m) mod 32 of each slot), but walks the set
+  // bits of its row of the screen bitmap; a column's counter counts its
+  // FLAGGED visits, and a visit waits until the flagged visits that precede it
+  // in that column's order (halves k+1 .. k+m, read off the column's bitmap
+  // row) have released it.  The two halves of a warp advance independently:
+  // a half whose next visit is not ready idles for one round (an exact
+  // identity inside rot_half) instead of blocking its sibling, so the walk
+  // cannot deadlock.  Same pairs, same per-column and per-half order as the
+  // unscreened phase restricted to the flagged pairs: deterministic.
+  __device__ void cross_screened(HCol<HR>& pc, double& np, double& dp, int sp, int sq0, int sq1, int sq2, int S,
+                                 Smem& sm) {
+    const unsigned full = 0xffffffffu;
+    const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
+    const int base = threadIdx.x & 16;
+    bool any = false;
+    if (threadIdx.x < 3 * 32) sm.qcnt[threadIdx.x] = 0;
+    __syncthreads();
+    const long long tc0 = prof_clock();
+    const int po = opos(sp * JB + hw), pw = opos(sp * JB) >> 5;  // my row, and the P block's bitmap word
+    // pending visits per slot: bit m <-> column (hw + m) mod 32
+    auto pend = [&](int sq) {
+      const unsigned row = sm.pbits[po][opos(sq * JB) >> 5];
+      return __funnelshift_r(row, row, hw);
+    };
+    unsigned r0 = pend(sq0), r1 = S > 1 ? pend(sq1) : 0u, r2 = S > 2 ? pend(sq2) : 0u;
+    const unsigned cp = sm.chg[sp * JB + hw];
+    while (__any_sync(full, (r0 | r1 | r2) != 0u)) {
+      int m = 32, x = 0;
+      if (r0) m = __ffs((int)r0) - 1;
+      if (r1 && __ffs((int)r1) - 1 < m) {
+        m = __ffs((int)r1) - 1;
+        x = 1;
+      }
+      if (r2 && __ffs((int)r2) - 1 < m) {
+        m = __ffs((int)r2) - 1;
+        x = 2;
+      }
+      const bool want = m < 32;
+      const int c = want ? (hw + m) & 31 : 0;
+      const int sq = x == 0 ? sq0 : (x == 1 ? sq1 : sq2);
+      int* cnt = &sm.qcnt[x * 32 + c];
+      // flagged visits of column c that come before mine: halves hw+1 .. hw+m
+      int need = 0;
+      int ready = 0;
+      if (hl == 0 && want) {
+        const unsigned col = sm.pbits[opos(sq * JB + c)][pw];
+        need = __popc(__funnelshift_r(col, col, (hw + 1) & 31) & ((1u << m) - 1u));
+        ready = ld_acquire(cnt) >= need;
+      }
+      need = __shfl_sync(full, need, base);
+      const bool valid = __shfl_sync(full, ready, base) != 0;
+      __syncwarp();  // lane 0's acquire is shared with its half before the column loads
+      if (!__any_sync(full, valid)) continue;  // neither half can go yet: look again
+      if (valid) {
+        const unsigned bit = ~(1u << m);
+        if (x == 0) r0 &= bit;
+        else if (x == 1) r1 &= bit;
+        else r2 &= bit;
+      }
+      const unsigned cq = sm.chg[sq * JB + c];
+      const double tl2 = (cp & cq & 4) ? kTailTol2 : tol2;
+      HCol<HR> q;
+      const uint32_t aq = scol(sq, c);
+      hcol_lds(q, aq);  // unconditional: an idle half applies the exact identity
+      double nq = valid ? sm.nrm[sq * JB + c] : 0.0, dq = sm.dsc[sq * JB + c];
+      const double npo = np;
+      const bool rr = rot_half<HR, true>(pc, q, 0u, aq, np, nq, dp, dq, valid, tl2, offmax);
+      if (!valid) np = npo;
+      if (rr) {
+        any = true;
+        if (hl == 0) {
+          sm.nrm[sq * JB + c] = nq;
+          sm.dsc[sq * JB + c] = dq;
+          sm.chg[sp * JB + hw] |= 2;
+          sm.chg[sq * JB + c] |= 2;
+        }
+      }
+      __syncwarp();  // the half's column stores are ordered before lane 0's release
+      if (hl == 0 && valid) st_release(cnt, need + 1);
+    }
+    __syncthreads();
+    if (__any_sync(full, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
     if (threadIdx.x == 0 && TB_PROF && sm.prof) atomicAdd(&sm.prof[14], (unsigned long long)(prof_clock() - tc0));
   }
 
@@ -3689,7 +3781,7 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
     sm.prof = prof;
     sm.kcut = (kcut > 0 && kcut < K) ? kcut : MAXDIM;
     sm.tmem_on = (precond >> 1) & 1;
-    sm.screen_on = (precond >> 4) & 1;
+    sm.screen_on = ((precond >> 4) & 1) + ((precond >> 7) & 1);
     sm.maxsweep = MAXSWEEP;
     sm.inject = 0;
     sm.sample = 0;

@@ -55,6 +55,16 @@ def test_tmem_qrcp_svd_matches_lapack(engine, monkeypatch, m, n, tmem):
     _check_svd(engine, m, n)
 
 
+# Gram screen of the late Jacobi sweeps (DMMA Gram matrix, flagged pairs only):
+# off (0), screened visits (1), + flag-driven cross phases (2, the default);
+# shapes with 2..4 column blocks and 64 / 128 rows, ragged ones included
+@pytest.mark.parametrize("m,n", [(128, 128), (64, 128), (128, 64), (64, 64), (100, 77), (128, 96), (72, 128)])
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_gram_screen_svd_matches_lapack(engine, monkeypatch, m, n, mode):
+    monkeypatch.setenv("TB_GRAM_SCREEN", mode)
+    _check_svd(engine, m, n)
+
+
 def _check_svd(engine, m, n):
     rng = np.random.default_rng(m * 1000 + n)
     k = min(m, n)

@@ -22,6 +22,12 @@ bounds any per-sample comparison once truncation is chaotic.
         table is written to gpurun_out/truncated_stats_<config>.txt;
   plus the cumulative discarded weight while < 1e-8: 5% relative (its
   per-update (total - kept)/total carries ~1e-16 cancellation noise).
+
+Two modes per config: "headline" (pi_local=True, what bench.py runs) and
+"faithful" (pi_local=False: ring-bond pi gates take the reference's truncating
+swap sweep).  In the headline mode the prefixes that hold a ring-bond pi gate
+are outside (i) and (iii) — there the engine runs a different, documented
+algorithm — and are covered by (ii); the faithful mode compares every sample.
 """
 
 import math
@@ -37,13 +43,13 @@ DELTA = math.pi / 2**7
 CFG = {"c2": (16, 2, 3, 32), "c3": (32, 4, 5, 64)}
 
 
-def _pipeline_values(name, n_ref):
+def _pipeline_values(name, n_ref, pi_local=True):
     n, hs, cs, chi = CFG[name]
     ham = tb.build_spin_ring(n, 1.0, hs)
     cfg = tb.PaiConfig(DELTA, 200, 2.0)
     ck = np.arange(10, 201, 10)
     pipe = tb.SlotPipeline(ham, cfg, cs, "01" * (n // 2), tb.TruncationPolicy(chi, 1e-12), ck, n_slots=296,
-                           pi_local=True)
+                           pi_local=pi_local)
     vals = np.full((n_ref, ck.size, n), np.nan)
     disc = np.full((n_ref, ck.size), np.nan)
     sign = np.zeros((n_ref, ck.size), np.int64)
@@ -78,15 +84,16 @@ def _ring_pi_prefixes(name, S):
     return out
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
-def test_headline_mode_truncated_statistics(engine, golden, name):
+@pytest.mark.parametrize("name,pi_local", [("c2", True), ("c3", True), ("c2", False), ("c3", False)],
+                         ids=["c2-headline", "c3-headline", "c2-faithful", "c3-faithful"])
+def test_headline_mode_truncated_statistics(engine, golden, name, pi_local):
     from conftest import GOLDEN
     if not os.path.exists(os.path.join(GOLDEN, f"ref_{name}_stat.npz")):
         pytest.skip(f"ref_{name}_stat.npz not generated (tests/golden/make_golden_trunc.py --only {name})")
     ref = golden(f"ref_{name}_stat.npz")
     r1, r2 = ref["vals_gesdd"], ref["vals_gesvd"]
     S = r1.shape[0]
-    vals, disc, sign = _pipeline_values(name, S)
+    vals, disc, sign = _pipeline_values(name, S, pi_local)
     assert not np.isnan(vals).any()
     np.testing.assert_array_equal(sign, ref["sign"])
 
@@ -97,7 +104,7 @@ def test_headline_mode_truncated_statistics(engine, golden, name):
     # left to (ii) and (iii).
     early = ref["disc_gesdd"] < 1e-8
     assert early[:, 0].all() and early.sum() >= S  # at least the first checkpoint of every sample
-    ring_pi = _ring_pi_prefixes(name, S)
+    ring_pi = _ring_pi_prefixes(name, S) if pi_local else np.zeros_like(early)
     same = early & ~ring_pi
     diff = np.abs(vals - r1)
     assert diff[same].max() <= 1e-8, diff[same].max()
@@ -118,8 +125,11 @@ def test_headline_mode_truncated_statistics(engine, golden, name):
     # later seed than that of an independent SVD algorithm.  The comparison
     # therefore allows the reference's own spread of the NEXT checkpoint:
     # quantile_GPU(c) <= 3 * max(quantile_ref(c), quantile_ref(c + 1)).
+    # In the headline mode the prefixes that hold a ring-bond pi gate follow a
+    # different (documented) algorithm than the reference, so they are left to
+    # (ii); the faithful mode (pi_local=False) compares every sample.
     self_spread = np.abs(r2 - r1)
-    late = ~early
+    late = ~early & ~ring_pi
     C = r1.shape[1]
     rows = []
     for c in range(C):
@@ -133,8 +143,9 @@ def test_headline_mode_truncated_statistics(engine, golden, name):
         rows.append((c, int(m.sum())) + tuple(float(np.percentile(x, q)) for q in (50, 90) for x in (g, rr, rn)))
     out = os.environ.get("TB_STATS_TABLE_DIR", "gpurun_out")
     if os.path.isdir(out):
-        with open(os.path.join(out, f"truncated_stats_{name}.txt"), "w") as fh:
-            fh.write(f"# {name}: per checkpoint, samples past the untruncated prefix; |GPU - ref| vs |gesvd - gesdd| "
+        mode = "headline" if pi_local else "faithful"
+        with open(os.path.join(out, f"truncated_stats_{name}_{mode}.txt"), "w") as fh:
+            fh.write(f"# {name}, {mode} mode (pi_local={pi_local}): per checkpoint, samples past the untruncated prefix; |GPU - ref| vs |gesvd - gesdd| "
                      "at the same and at the next checkpoint\n# ckpt n  gpu50 ref50 ref50_next  gpu90 ref90 ref90_next\n")
             for r in rows:
                 fh.write("%2d %3d  %.3e %.3e %.3e  %.3e %.3e %.3e\n" % r)

@@ -236,6 +236,12 @@ int validate_desc(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o
   return TB_OK;
 }
 
+// TB_GRAM_SCREEN: 0 = off, 1 = late sweeps visit only the pairs flagged by the
+// DMMA Gram screen, 2 = + flag-driven cross phases (default), 3 = + flag-driven
+// within-block phases (measured slightly slower than 2: 1.786 vs 1.812
+// samples/s, profiles/r02v_bench_*.json)
+constexpr int kGramScreenDefault = 2;
+
 tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o) {
   tb::Job job;
   memset(&job, 0, sizeof(job));
@@ -251,7 +257,7 @@ tb::Job make_job(tb_ctx* c, const tb_ensemble_desc* d, const tb_ensemble_out* o)
     const char* tm = getenv("TB_QRCP_TMEM");
     job.qrcp_tmem = tm ? atoi(tm) : 1;
     const char* gs = getenv("TB_GRAM_SCREEN");
-    job.gram_screen = gs ? atoi(gs) : 2;  // 0: off, 1: screened visits, 2: + flag-driven cross phases
+    job.gram_screen = gs ? atoi(gs) : kGramScreenDefault;
     const char* ms = getenv("TB_MAX_SWEEPS");
     job.max_sweeps = ms ? atoi(ms) : tb::MAXSWEEP;
     if (job.max_sweeps < 1 || job.max_sweeps > tb::MAXSWEEP) job.max_sweeps = tb::MAXSWEEP;
@@ -762,7 +768,7 @@ int tb_svd_trunc(tb_ctx* c, const double* a, int64_t batch, int64_t m, int64_t n
   const char* ct = getenv("TB_CLUSTER_TMA");
   const char* gs = getenv("TB_GRAM_SCREEN");
   const int precond = (pe ? atoi(pe) : 1) | ((!tm || atoi(tm)) ? 2 : 0) | (clu ? 4 : 0) | ((!ct || atoi(ct)) ? 8 : 0) |
-                      ((!gs || atoi(gs)) ? 16 : 0) | ((!gs || atoi(gs) > 1) ? 128 : 0) | ((getenv("TB_CL_DBG") ? atoi(getenv("TB_CL_DBG")) & 3 : 0) << 5);
+                      ((!gs || atoi(gs)) ? 16 : 0) | (((gs ? atoi(gs) : kGramScreenDefault) - 1) & 3) << 7 | ((getenv("TB_CL_DBG") ? atoi(getenv("TB_CL_DBG")) & 3 : 0) << 5);
   if (clu) {
     TB_CUDA(c, cudaFuncSetAttribute(tb::svd_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};

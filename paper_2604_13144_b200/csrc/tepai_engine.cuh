@@ -622,6 +622,9 @@ __device__ __forceinline__ void half_sum8(double (&v)[8]) {
 }
 
 constexpr double kTailTol2 = 1e-8;  // (relative coupling 1e-4)^2 for pairs of two tail columns
+#ifndef TB_GRAM_UNROLL
+#define TB_GRAM_UNROLL 2  // k-steps of the Gram loop in flight (4: measured)
+#endif
 constexpr double kScreenOn = 1e-2;  // Gram-screen the next sweep once a sweep's largest rotated coupling^2 is below this
 
 // ----------------------------------------------------------------------------
@@ -824,7 +827,11 @@ struct JacobiH {
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b) cre[a][b][0] = cre[a][b][1] = cim[a][b][0] = cim[a][b][1] = 0.0;
+#if TB_GRAM_UNROLL == 4
+#pragma unroll 4
+#else
 #pragma unroll 2
+#endif
       for (int k0 = 0; k0 < LD; k0 += 4) {
         const int row = k0 + fk;
         double2 x[2], y[2];
@@ -888,7 +895,133 @@ struct JacobiH {
   // most 16 pairs).  For ns >= 2 the two slot-rounds of a step touch
   // different slots, and a slot's consecutive rounds (m, m + ns) always fall
   // in different steps, so one barrier per step orders everything.
+  // Within-block phase of a SCREENED sweep: the flagged pairs of the round
+  // robin only, ordered by per-column counters instead of one CTA barrier per
+  // round.  Half (g, p) (g = hw / 16, p = hw % 16) owns position p of the
+  // circle method in the slot-rounds with (round + slot) odd/even = g and walks
+  // them in increasing round order; a pair runs once the flagged pairs of BOTH
+  // its columns from earlier rounds have released them (a column's counter
+  // counts its flagged visits; the number that precede a round is read off the
+  // column's bitmap row with the inverse of the circle method).  A column's
+  // pairs therefore run in round order, exactly as in within(), and a wait
+  // always points to a strictly earlier round, so the walk cannot deadlock;
+  // the two halves of a warp advance independently as in cross_screened.
+  __device__ __forceinline__ static int rr_round(int i, int j, int Np) {
+    const int m = Np - 1;  // odd
+    if (i == m) return j;
+    if (j == m) return i;
+    return ((i + j) * ((m + 1) >> 1)) % m;
+  }
+  __device__ void within_screened(int s0, int s1, int s2, int ns, Smem& sm) {
+    const unsigned full = 0xffffffffu;
+    const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
+    const int base = threadIdx.x & 16, g = hw >> 4, p = hw & 15;
+    bool any = false;
+    if (threadIdx.x < 3 * 32) sm.qcnt[threadIdx.x] = 0;
+    __syncthreads();
+    int rounds = 0;
+    for (int x = 0; x < ns; ++x) {
+      const int nb = sm.jncol[x == 0 ? s0 : (x == 1 ? s1 : s2)];
+      rounds = max(rounds, nb + (nb & 1) - 1);
+    }
+    // scan position: slot-rounds in (round, slot) order
+    int r = 0, x = 0;
+    bool want = false;
+    int s = 0, i = 0, j = 0, nbp = 2;
+    auto advance = [&]() {  // next flagged pair of this half at or after (r, x); want = false when exhausted
+      want = false;
+      while (r < rounds) {
+        if (((r + x) & 1) == g) {
+          s = (x == 0) ? s0 : (x == 1 ? s1 : s2);
+          const int nb = sm.jncol[s];
+          nbp = nb + (nb & 1);
+          if (r < nbp - 1 && p < nbp / 2) {
+            rr_pair(r, p, nbp, i, j);
+            if (i < nb && j < nb && flagged(sm, s * JB + i, s * JB + j)) {
+              want = true;
+              return;
+            }
+          }
+        }
+        if (++x == ns) {
+          x = 0;
+          ++r;
+        }
+      }
+    };
+    auto step = [&]() {
+      if (++x == ns) {
+        x = 0;
+        ++r;
+      }
+    };
+    advance();
+    while (__any_sync(full, want)) {
+      // flagged pairs of column i (and of column j) in earlier rounds: lanes check partners hl and hl + 16
+      const int nb = sm.jncol[s];
+      int need_i = 0, need_j = 0;
+      {
+        const int ci = opos(s * JB + i), cj = opos(s * JB + j);
+        const unsigned rowi = sm.pbits[ci][ci >> 5], rowj = sm.pbits[cj][cj >> 5];
+        bool bi0 = false, bi1 = false, bj0 = false, bj1 = false;
+        if (want) {
+          const int a = hl, b = hl + 16;
+          bi0 = a < nb && a != i && ((rowi >> a) & 1u) && rr_round(i, a, nbp) < r;
+          bi1 = b < nb && b != i && ((rowi >> b) & 1u) && rr_round(i, b, nbp) < r;
+          bj0 = a < nb && a != j && ((rowj >> a) & 1u) && rr_round(j, a, nbp) < r;
+          bj1 = b < nb && b != j && ((rowj >> b) & 1u) && rr_round(j, b, nbp) < r;
+        }
+        const unsigned hm = 0xFFFFu << base;
+        need_i = __popc(__ballot_sync(full, bi0) & hm) + __popc(__ballot_sync(full, bi1) & hm);
+        need_j = __popc(__ballot_sync(full, bj0) & hm) + __popc(__ballot_sync(full, bj1) & hm);
+      }
+      int* cnti = &sm.qcnt[(s < 3 ? s : 0) * 32 + i];
+      int* cntj = &sm.qcnt[(s < 3 ? s : 0) * 32 + j];
+      int ready = 0;
+      if (hl == 0 && want) ready = ld_acquire(cnti) >= need_i && ld_acquire(cntj) >= need_j;
+      const bool valid = __shfl_sync(full, ready, base) != 0;
+      __syncwarp();
+      if (!__any_sync(full, valid)) continue;  // neither half can go yet
+      const unsigned ci8 = sm.chg[s * JB + i], cj8 = sm.chg[s * JB + j];
+      const bool tt = (ci8 & cj8 & 4) != 0;
+      HCol<HR> a, b;
+      const uint32_t ai = scol(s, i), aj = scol(s, j);
+      hcol_lds(a, ai);
+      hcol_lds(b, aj);
+      double na = valid ? sm.nrm[s * JB + i] : 0.0, nb2 = valid ? sm.nrm[s * JB + j] : 0.0;
+      double da = sm.dsc[s * JB + i], db = sm.dsc[s * JB + j];
+      const bool rr = rot_half<HR, false>(a, b, ai, aj, na, nb2, da, db, valid, tt ? kTailTol2 : tol2, offmax);
+      if (rr) {
+        any = true;
+        if (hl == 0) {
+          sm.nrm[s * JB + i] = na;
+          sm.nrm[s * JB + j] = nb2;
+          sm.dsc[s * JB + i] = da;
+          sm.dsc[s * JB + j] = db;
+          sm.chg[s * JB + i] |= 2;
+          sm.chg[s * JB + j] |= 2;
+        }
+      }
+      __syncwarp();  // the half's column stores are ordered before lane 0's releases
+      if (valid) {
+        if (hl == 0) {
+          st_release(cnti, need_i + 1);
+          st_release(cntj, need_j + 1);
+        }
+        step();
+        advance();
+      }
+    }
+    __syncthreads();
+    if (__any_sync(full, any) && (threadIdx.x & 31) == 0) sm.flag = 1;
+    __syncthreads();
+  }
+
   __device__ void within(int s0, int s1, int s2, int ns, Smem& sm) {
+    if (screen && sm.screen_on > 2) {
+      within_screened(s0, s1, s2, ns, sm);
+      return;
+    }
     const int hw = threadIdx.x >> 4;  // half-warp id 0..31
     const int hl = threadIdx.x & 15;
     int rounds = 0;
@@ -3781,7 +3914,7 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const double2* a, int m, int
     sm.prof = prof;
     sm.kcut = (kcut > 0 && kcut < K) ? kcut : MAXDIM;
     sm.tmem_on = (precond >> 1) & 1;
-    sm.screen_on = ((precond >> 4) & 1) + ((precond >> 7) & 1);
+    sm.screen_on = ((precond >> 4) & 1) ? 1 + ((precond >> 7) & 3) : 0;  // 0 off, 1..3 (see TB_GRAM_SCREEN)
     sm.maxsweep = MAXSWEEP;
     sm.inject = 0;
     sm.sample = 0;

@@ -64,8 +64,17 @@ def _select_driver(driver: str):
         _kernel.np = np
         return
 
-    def svd(a, full_matrices=True):
-        return scipy.linalg.svd(a, full_matrices=full_matrices, lapack_driver="gesvd", check_finite=False)
+    if driver == "gesdd_t":
+        # zgesdd on the conjugate transpose: the same LAPACK driver, but an
+        # independent bidiagonalisation (zgesdd and zgesvd on the SAME matrix
+        # share zgebrd), i.e. a twin that differs from the shipped reference the
+        # way an independent SVD algorithm of the same accuracy class does
+        def svd(a, full_matrices=True):
+            u, sv, vh = np.linalg.svd(np.ascontiguousarray(a.conj().T), full_matrices=full_matrices)
+            return np.ascontiguousarray(vh.conj().T), sv, np.ascontiguousarray(u.conj().T)
+    else:
+        def svd(a, full_matrices=True):
+            return scipy.linalg.svd(a, full_matrices=full_matrices, lapack_driver="gesvd", check_finite=False)
 
     shim = types.SimpleNamespace(**{k: getattr(np, k) for k in dir(np) if not k.startswith("__")})
     shim.linalg = types.SimpleNamespace(svd=svd, qr=np.linalg.qr)
@@ -147,7 +156,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=max(1, (os.cpu_count() or 2) - 1))
     ap.add_argument("--only", choices=sorted(CONFIGS), default=None)
+    ap.add_argument("--third-twin", type=int, default=0, metavar="N",
+                    help="only run the first N samples of --only with zgesdd on the conjugate transpose and write "
+                         "ref_<config>_stat_twinT.npz (the spread an independent bidiagonalisation gives)")
     a = ap.parse_args()
+    if a.third_twin:
+        nm = a.only or "c3"
+        jobs = [(nm, i, "gesdd_t") for i in range(a.third_twin)]
+        with Pool(a.procs) as pool:
+            for k, p in enumerate(pool.imap_unordered(run_member, jobs, chunksize=1)):
+                print(f"[{k + 1}/{len(jobs)}] {os.path.basename(p)}", flush=True)
+        rows = [np.load(os.path.join(CACHE, f"{nm}_gesdd_t_{i}.npz")) for i in range(a.third_twin)]
+        np.savez_compressed(os.path.join(HERE, f"ref_{nm}_stat_twinT.npz"), sample_ids=np.arange(a.third_twin),
+                            vals_gesdd_t=np.stack([r["vals"] for r in rows]),
+                            disc_gesdd_t=np.stack([r["disc"] for r in rows]))
+        print("written:", f"ref_{nm}_stat_twinT.npz")
+        return
     names = [a.only] if a.only else ["c2", "c3"]
     purge_leaked(names)
     jobs = [(nm, i, d) for nm in names for i in range(CONFIGS[nm][6]) for d in ("gesdd", "gesvd")]
